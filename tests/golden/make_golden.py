@@ -1,0 +1,249 @@
+"""Generate the golden fixtures from the REAL reference implementation.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    python tests/golden/make_golden.py
+
+It imports ``pimpc`` from ``/root/reference/pkg/src`` (read-only, never
+copied), builds seeded inputs with ``paper_1503_00330_b200.synthetic``,
+calls the reference's own public API (``FrozenLwpr.predict_into``,
+``LwprModel.predict_batch``, ``RolloutEngine.evaluate``,
+``path_integral_update``, ``optimize``, ``receding_horizon_step``,
+``rng.derive_key``/``normal_block``, ``wrap_angle``) and writes the inputs
+and outputs to ``tests/golden/*.npz``.  The fixtures pin both the oracle
+(tests/test_oracle.py) and the CUDA path (tests/test_gpu_*.py).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg"
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "tests"))
+
+from pimpc import controller as C  # noqa: E402
+from pimpc import dynamics as D  # noqa: E402
+from pimpc import lwpr as LW  # noqa: E402
+from pimpc import rng as R  # noqa: E402
+from pimpc import simworld as S  # noqa: E402
+
+from paper_1503_00330_b200 import synthetic  # noqa: E402
+
+
+def ref_model(stack) -> LW.LwprModel:
+    m = LW.LwprModel(input_dim=stack.centers.shape[1])
+    for i in range(stack.num_fields):
+        m.fields.append(
+            LW.ReceptiveField(
+                center=stack.centers[i].copy(),
+                metric=stack.metrics[i].copy(),
+                coef=stack.coefs[i].copy(),
+                local_variance=float(stack.lvar[i]),
+                inv_gram=np.eye(stack.centers.shape[1] + 1),
+            )
+        )
+    m._stacked = None
+    return m
+
+
+def ref_hybrid(stacks) -> D.HybridModel:
+    return D.HybridModel(tuple(ref_model(s) for s in stacks), D.QuadParams())
+
+
+def stack_arrays(prefix, stacks):
+    out = {}
+    for a, s in enumerate(stacks):
+        out[f"{prefix}centers{a}"] = s.centers
+        out[f"{prefix}metrics{a}"] = s.metrics
+        out[f"{prefix}coefs{a}"] = s.coefs
+        out[f"{prefix}lvar{a}"] = s.lvar
+    return out
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} B)")
+
+
+def far_stacks(num_fields=4):
+    """A model whose kernels are so narrow that many rollout rows have every
+    weight denormal (exp in (-103.97, -87.3)) or zero (0/0 = NaN → cost
+    ceiling + crash flag): the FP32 underflow semantics of SURVEY.md §0.9."""
+    base = synthetic.hybrid_stacks(num_fields, seed=11)
+    out = []
+    for s in base:
+        m = s.metrics.copy()
+        m[:, 3, 3] = 6.0e3
+        m[:, 0, 0] = m[:, 1, 1] = m[:, 2, 2] = 3.0e2
+        out.append(synthetic.AxisStack(s.centers, m, s.coefs, s.lvar))
+    return tuple(out)
+
+
+def make_lwpr():
+    rng = np.random.default_rng(123)
+    arrays = {}
+    # (1) synthetic diagonal-metric axis models, FP32 fast path + FP64 path
+    stacks = synthetic.hybrid_stacks(24, seed=5)
+    X = rng.uniform([-0.6, -0.6, -0.6, 0.0], [0.6, 0.6, 0.6, 0.37], size=(257, 4)).astype(np.float32)
+    arrays["diag_X"] = X
+    arrays.update(stack_arrays("diag_", stacks))
+    for a, s in enumerate(stacks):
+        m = ref_model(s)
+        fr = LW.FrozenLwpr(m, batch_rows=X.shape[0])
+        assert fr._diagonal_only
+        mean = np.empty(X.shape[0], np.float32)
+        var = np.empty(X.shape[0], np.float32)
+        fr.predict_into(X, mean, var)
+        arrays[f"diag_mean{a}"], arrays[f"diag_var{a}"] = mean, var
+        m64, v64 = m.predict_batch(X.astype(np.float64))
+        arrays[f"diag_mean64_{a}"], arrays[f"diag_var64_{a}"] = m64, v64
+    # (2) full SPD metrics of random dimension (reference tests/oracles.py:47-67)
+    from oracles import random_small_model
+
+    r2 = np.random.default_rng(21)
+    for i in range(8):
+        m = random_small_model(r2)
+        c, mt, cf, lv = m._stacks()
+        Xf = r2.normal(size=(64, m.input_dim)).astype(np.float32)
+        fr = LW.FrozenLwpr(m, batch_rows=64)
+        mean = np.empty(64, np.float32)
+        var = np.empty(64, np.float32)
+        fr.predict_into(Xf, mean, var)
+        arrays.update({f"full{i}_centers": c, f"full{i}_metrics": mt, f"full{i}_coefs": cf,
+                       f"full{i}_lvar": lv, f"full{i}_X": Xf, f"full{i}_mean": mean,
+                       f"full{i}_var": var, f"full{i}_diag": np.array(fr._diagonal_only)})
+    # (3) scalar hand cases of tests/test_lwpr.py:54-67 via the scalar oracle
+    arrays["n_full"] = np.array(8)
+    save("lwpr", **arrays)
+
+
+def evaluate_case(name, stacks, K, N, M, seed, cycle, waypoint, state_pos=None,
+                  plan_thrust=None, chunk=7, std=(2.0, 2.0, 0.8, 0.05)):
+    p = D.QuadParams()
+    model = D.AnalyticModel(p) if stacks is None else ref_hybrid(stacks)
+    task = S.Task.default()
+    cfg = C.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1,
+                     exploration_std=np.array(std), rng_seed=seed, chunk_size=chunk)
+    state = D.QuadState.hover(task.spawn if state_pos is None else np.asarray(state_pos, float))
+    plan = C.ControlPlan.hover(p, N)
+    if plan_thrust is not None:
+        plan = plan.replaced(np.tile([0.0, 0.0, 0.0, plan_thrust], (N, 1)))
+    noise = C.sample_noise(cfg, cycle, 0)
+    engine = C.RolloutEngine(model, cfg)
+    dyn = C.sample_dynamics_noise(cfg, cycle, 0) if engine.use_spread else None
+    batch = engine.evaluate(state, plan, noise, S.RolloutCost(task, waypoint), dyn)
+    new_plan = C.path_integral_update(plan, batch, cfg.temperature)
+    arrays = dict(
+        K=np.array(K), N=np.array(N), M=np.array(M), seed=np.array(seed), cycle=np.array(cycle),
+        waypoint_index=np.array(waypoint), analytic=np.array(stacks is None),
+        state=state.as_array(), plan=plan.controls, noise=noise,
+        dyn=dyn if dyn is not None else np.zeros((0,), np.float32),
+        std=np.array(std), costs=batch.costs_to_go, crash=batch.crash_flags,
+        new_plan=new_plan.controls, temperature=np.array(cfg.temperature),
+        ceiling=np.array(cfg.cost_ceiling),
+    )
+    if stacks is not None:
+        arrays.update(stack_arrays("", stacks))
+    save("eval_" + name, **arrays)
+    return batch
+
+
+def make_eval():
+    evaluate_case("hybrid_m1", synthetic.hybrid_stacks(16, seed=1), K=64, N=20, M=1,
+                  seed=0, cycle=0, waypoint=1)
+    evaluate_case("hybrid_m4", synthetic.hybrid_stacks(16, seed=2), K=48, N=15, M=4,
+                  seed=3, cycle=2, waypoint=0)
+    evaluate_case("hybrid_m3", synthetic.hybrid_stacks(12, seed=3), K=40, N=12, M=3,
+                  seed=4, cycle=1, waypoint=2)
+    evaluate_case("hybrid_m6", synthetic.hybrid_stacks(12, seed=4), K=24, N=10, M=6,
+                  seed=5, cycle=0, waypoint=1)
+    evaluate_case("full_m2", synthetic.hybrid_stacks(10, seed=6, full_metric=True), K=32, N=10,
+                  M=2, seed=6, cycle=3, waypoint=0)
+    evaluate_case("analytic", None, K=64, N=25, M=1, seed=7, cycle=1, waypoint=0,
+                  state_pos=np.array([-1.0, -0.7, 1.1]), std=(1.5, 1.5, 0.6, 0.04))
+    b = evaluate_case("far_m1", far_stacks(), K=64, N=30, M=1, seed=8, cycle=0, waypoint=1,
+                      std=(4.0, 4.0, 1.5, 0.08))
+    print("far_m1: ceiling rows", int((b.costs_to_go == 1e8).any(axis=1).sum()))
+    b = evaluate_case("far_m4", far_stacks(), K=32, N=24, M=4, seed=9, cycle=0, waypoint=1,
+                      std=(4.0, 4.0, 1.5, 0.08))
+    print("far_m4: ceiling rows", int((b.costs_to_go == 1e8).any(axis=1).sum()))
+    b = evaluate_case("crash_m1", synthetic.hybrid_stacks(16, seed=10), K=64, N=30, M=1,
+                      seed=10, cycle=0, waypoint=0, state_pos=np.array([-1.1, -0.9, 0.3]),
+                      plan_thrust=0.175)
+    print("crash_m1: crashed", int(b.crash_flags.sum()))
+
+
+def make_update():
+    arrays = {}
+    # hand softmax (test_controller.py:213-223)
+    noise = np.zeros((2, 3, 4))
+    noise[0] += 0.02
+    noise[1] -= 0.02
+    costs = np.vstack([np.ones(3), 2.0 * np.ones(3)])
+    plan = C.ControlPlan.hover(D.QuadParams(), 3)
+    arrays["hand_noise"], arrays["hand_costs"], arrays["hand_plan"] = noise, costs, plan.controls
+    arrays["hand_new"] = C.path_integral_update(
+        plan, C.RolloutBatch(noise, costs, np.zeros(2, bool)), 1.0).controls
+    # random batches at several temperatures, incl. huge cost spreads
+    r = np.random.default_rng(77)
+    for i, (k, n, lam, scale) in enumerate([(30, 8, 2.0, 100.0), (257, 13, 0.05, 10.0),
+                                            (1000, 5, 1.0, 1e4), (3, 50, 1e3, 1.0)]):
+        costs = r.uniform(0, scale, size=(k, n))
+        noise = r.normal(size=(k, n, 4)) * np.array([2.0, 2.0, 0.8, 0.05])
+        plan = C.ControlPlan.hover(D.QuadParams(), n)
+        new = C.path_integral_update(plan, C.RolloutBatch(noise, costs, np.zeros(k, bool)), lam)
+        arrays.update({f"r{i}_costs": costs, f"r{i}_noise": noise, f"r{i}_plan": plan.controls,
+                       f"r{i}_lambda": np.array(lam), f"r{i}_new": new.controls})
+    arrays["n_random"] = np.array(4)
+    save("update", **arrays)
+
+
+def make_optimize():
+    stacks = synthetic.hybrid_stacks(16, seed=12)
+    p = D.QuadParams()
+    model = ref_hybrid(stacks)
+    task = S.Task.default()
+    cfg = C.PiConfig(num_rollouts=64, sub_rollouts=4, horizon_steps=20, iterations_per_step=2,
+                     rng_seed=3, chunk_size=16)
+    state = D.QuadState.hover(task.spawn + np.array([0.05, -0.02, 0.03]))
+    plan = C.ControlPlan.hover(p, 20)
+    cost = S.RolloutCost(task, 1)
+    opt = C.optimize(state, plan, cfg, model, cost, cycle_index=5)
+    ctrl, carried = C.receding_horizon_step(state, plan, cfg, model, cost, cycle_index=5)
+    save("optimize", **stack_arrays("", stacks), state=state.as_array(), plan=plan.controls,
+         K=np.array(64), M=np.array(4), N=np.array(20), iterations=np.array(2), seed=np.array(3),
+         cycle=np.array(5), waypoint_index=np.array(1), optimized=opt.controls,
+         control=ctrl.as_array(), carried=carried.controls)
+
+
+def make_rng():
+    coords = [(0,), (1, 0, 0), (1, 3, 1), (2, 7, 0), (3, 2**40, 5), (1, 2**64 - 1, 2)]
+    seeds = [0, 1, 8, 2**63 + 5]
+    keys = np.array([[R.derive_key(s, *c) for c in coords] for s in seeds], dtype=np.uint64)
+    sm = np.array([R.splitmix64(v) for v in [0, 1, 2**64 - 1, 0x123456789ABCDEF]], np.uint64)
+    blk = R.normal_block(8, (1, 3, 1), (3, 4, 4))
+    blk32 = R.normal_block(8, (2, 3, 1), (2, 3, 4, 3), dtype=np.float32)
+    angles = np.array([0.0, np.pi, -np.pi, 3 * np.pi, -3 * np.pi, 1e-300, -1e-300, 7.5, -7.5,
+                       np.nextafter(np.pi, 4), np.nextafter(-np.pi, -4), 100.0, -100.0,
+                       2 * np.pi, -2 * np.pi, 1e6, 1.0e-17])
+    save("rng", coords_len=np.array([len(c) for c in coords]), keys=keys, splitmix=sm,
+         seeds=np.array(seeds, dtype=np.uint64), normal_block=blk, normal_block32=blk32,
+         angles=angles, wrapped=D.wrap_angle(angles))
+
+
+if __name__ == "__main__":
+    make_rng()
+    make_lwpr()
+    make_eval()
+    make_update()
+    make_optimize()
