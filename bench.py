@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""PI²-RH control-step benchmark (BASELINE.json metric: rollout-steps/s = K x T LWPR predicts).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one receding-horizon control step with iterations_per_step=1 on the
+named workload (default C2: K=65536 rollouts, T=50, L=100 receptive fields per
+axis, M=4 sub-rollouts — "uncertainty penalty on"), synthetic
+hybrid-LWPR model (paper_1503_00330_b200.synthetic), device-generated noise.
+
+* value: K*T*steps / device time of `steps` back-to-back iterations whose state,
+  plan and model are already resident in HBM (CUDA events on the launch stream,
+  barrier + synchronize on both sides, max over ranks).
+* e2e: the same metric through the public API `receding_horizon_step(...)`
+  with host state/plan in and host control/plan out (H2D + D2H inside).
+* roofline: the LWPR kernel (dominant) — algorithmic FP32 FLOPs per launch over
+  its CUDA-event duration vs the FP32 CUDA-core peak.
+* cpu_baseline / --impl reference: the reference algorithm (numpy oracle port,
+  oracle/) on the host cores, on a bounded sample of the same workload.
+
+Under torchrun (N > 1) rollouts are sharded across ranks (strong scaling) and the
+per-timestep softmax partials are all-gathered over NCCL.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rollout-steps/sec (K×T LWPR predicts)"
+UNIT = "rollout-steps/s"
+KERNELS_PER_ITER = 5  # attitude, lwpr, rollout, partials, combine
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--cpu-sample", type=int, default=4096, help="rollouts in the CPU baseline sample")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload(name: str):
+    from paper_1503_00330_b200.synthetic import CONFIGS
+
+    c = dict(CONFIGS[name])
+    desc = {
+        "C1": "single PI²-RH control step, K=1024, T=50, L=100, M=1",
+        "C2": "quadrotor obstacle-navigation step, K=65536, T=50, L=100, uncertainty on (M=4 sub-rollouts)",
+        "C3": "large LWPR L=1000, K=262144, T=100, M=1",
+        "C4": "K=2^20, T=50, L=100, M=1 control step",
+        "C5": "K=2^22, T=50, L=200, M=1",
+    }[name]
+    return c, desc
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(cfgd, sample_k: int, min_seconds: float, max_steps: int | None = None):
+    """Reference algorithm (oracle port) on the host cores: one optimisation iteration
+    (sample_noise [+ dyn] + evaluate + update) per step on a bounded sample."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import rollout as RO
+    from paper_1503_00330_b200 import synthetic
+
+    T, L, M = cfgd["T"], cfgd["L"], cfgd["M"]
+    k = min(sample_k, cfgd["K"])
+    workers = RO.default_workers()
+    chunk = min(1024, -(-k // workers))
+    model = RO.Model(synthetic.hybrid_stacks(L, seed=0))
+    cost = RO.Cost(synthetic.DEFAULT_WAYPOINTS[1], synthetic.DEFAULT_OBSTACLES)
+    state = np.zeros(12)
+    state[0:3] = synthetic.DEFAULT_WAYPOINTS[0]
+    plan = np.tile([0.0, 0.0, 0.0, model.dyn.hover_thrust], (T, 1))
+    times = []
+    with threadpool_limits(1, "blas"):
+        RO.optimize(model, state, plan, cost, K=k, M=M, iterations=1, chunk=chunk, workers=workers)  # warm-up
+        t_all = time.perf_counter()
+        cyc = 0
+        while True:
+            t0 = time.perf_counter()
+            RO.optimize(model, state, plan, cost, K=k, M=M, iterations=1, chunk=chunk, workers=workers,
+                        cycle=cyc)
+            times.append(time.perf_counter() - t0)
+            cyc += 1
+            if max_steps is not None and cyc >= max_steps:
+                break
+            if max_steps is None and (time.perf_counter() - t_all >= min_seconds and cyc >= 2):
+                break
+    step = statistics.median(times)
+    return {
+        "value": k * T / step,
+        "unit": UNIT,
+        "cores": workers,
+        "kind": "port",
+        "sample": f"K={k} of {cfgd['K']} rollouts, T={T}, L={L}, M={M}; numpy oracle (oracle/rollout.py), "
+                  f"{workers} worker threads, BLAS 1 thread; median of {len(times)} steps "
+                  f"(noise + evaluate + update)",
+        "ms_per_step": step * 1e3,
+        "step_times_s": times,
+    }
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (SM clock, max clock, throttle reasons)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=1)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- ours
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def lwpr_traffic(config: str):
+    """dram bytes per LWPR launch from a committed `ncu --set full` capture, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "lwpr_traffic.json")))
+        return d.get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args, rank: int, world: int, local: int):
+    import torch
+
+    import paper_1503_00330_b200 as P
+    from paper_1503_00330_b200 import _abi, synthetic
+    from paper_1503_00330_b200.controller import dynamics_struct, optimize_args
+    from paper_1503_00330_b200.simworld import cost_struct
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    cfgd, desc = workload(args.config)
+    K, T, L, M = cfgd["K"], cfgd["T"], cfgd["L"], cfgd["M"]
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=0), params)
+    task = P.Task.default()
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=T, iterations_per_step=1, rng_seed=0)
+    state = P.QuadState.hover(task.spawn)
+    plan0 = P.ControlPlan.hover(params, T)
+    cost = P.RolloutCost(task, 1)
+    stream = torch.cuda.current_stream(local)
+    sptr = _abi.ptr(stream.cuda_stream)
+
+    if world > 1:
+        from paper_1503_00330_b200.distributed import ShardedEngine, gather_partials
+
+        eng = ShardedEngine(model, cfg, device=local)
+        ctx = eng.ctx
+        k_local = eng.stop - eng.start
+    else:
+        eng = P.RolloutEngine(model, cfg, device=local, noise="device", use_graph=True)
+        ctx = eng.context(K, T)
+        k_local = K
+    ctx.call("pi2_set_dynamics", dynamics_struct(params, plan0.lo, plan0.hi))
+    ctx.call("pi2_set_cost", cost_struct(cost))
+    ctx.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan0.controls)), sptr)
+    partial = torch.empty((T, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=f"cuda:{local}")
+
+    def device_step(cycle):
+        a = optimize_args(cfg, cycle, use_graph=False)
+        ctx.call("pi2_iterate_local", a, 0, _abi.ptr(partial), sptr)
+        g = gather_partials(partial) if world > 1 else partial
+        ctx.call("pi2_iterate_finalize", _abi.ptr(g), world, float(cfg.temperature), sptr)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident throughput (value)
+    for w in range(args.warmup):
+        device_step(10_000 + w)
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for s in range(args.steps):
+            device_step(s)
+        end.record(stream)
+        barrier()
+    dev_ms = max_over_ranks(start.elapsed_time(end))
+    ms_per_step = dev_ms / args.steps
+    value = K * T * args.steps / (dev_ms / 1e3)
+
+    # ---- stage profile (dominant kernel = LWPR), CUDA events on the context stream
+    stage_ms = (_abi.C.c_double * 5)()
+    ctx.call("pi2_profile_iteration", optimize_args(cfg, 0, use_graph=False), 10, stage_ms)
+    stages = dict(zip(["attitude", "lwpr", "rollout_cost", "partials", "combine"], list(stage_ms)))
+
+    # ---- end to end through the public API (host state/plan in, control/plan out)
+    plan = plan0
+    lat = []
+    if world > 1:
+        for w in range(args.warmup):
+            eng.optimize(state, plan, cost, 10_000 + w)
+        barrier()
+        for s in range(args.steps):
+            t0 = time.perf_counter()
+            opt = eng.optimize(state, plan, cost, s)
+            ctrl, plan = opt.control_at(0), opt.shifted()
+            lat.append(time.perf_counter() - t0)
+    else:
+        for w in range(args.warmup):
+            P.receding_horizon_step(state, plan0, cfg, model, cost, 10_000 + w, eng)
+        barrier()
+        for s in range(args.steps):
+            t0 = time.perf_counter()
+            ctrl, plan = P.receding_horizon_step(state, plan, cfg, model, cost, s, eng)
+            lat.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(lat))
+    lat_ms = sorted(x * 1e3 for x in lat)
+    p50 = max_over_ranks(statistics.median(lat_ms))
+    p99 = max_over_ranks(lat_ms[min(len(lat_ms) - 1, math.ceil(0.99 * len(lat_ms)) - 1)])
+
+    if rank != 0:
+        return None
+
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_tflops = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
+    rows = k_local * T
+    flops_per_field = 32 if M > 1 else 27  # 27 (+5 variance) per (row, axis, field)
+    lwpr_flops = rows * 3 * L * flops_per_field
+    achieved = lwpr_flops / (stages["lwpr"] / 1e3) / 1e12
+    clk = clocks.summary()
+    peak_obs = n_sm * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12 if clk.get("sm_mhz") else None
+    h2d = 12 * 8 + T * 4 * 8 + 8 * (12 + 4 * 16 + 4 + 2) + 4 * 48  # state + plan + StepArgs
+    d2h = T * 4 * 8
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (LWPR, integration, cost) + f64 (attitude, cost-to-go, update)",
+        "data": "synthetic (seeded hybrid-LWPR model linearising the rigid-body quadrotor; device Philox noise)",
+        "config": {
+            "workload": f"{args.config}: {desc}",
+            "K": K, "T": T, "L": L, "M": M, "iterations_per_step": 1,
+            "parallelism": f"rollouts sharded over {world} GPU(s)",
+            "l2": "working set > L2 (xin+LWPR rows+costs ≈ %.0f MB per GPU)" % ((k_local * T * (16 + 32 + 8)) / 1e6),
+        },
+        "e2e": {
+            "value": K * T * args.steps / e2e_s,
+            "unit": UNIT,
+            "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "api": "paper_1503_00330_b200.receding_horizon_step(noise='device' engine)" if world == 1
+                   else "distributed.ShardedEngine.optimize",
+        },
+        "latency_ms": {"p50": p50, "p99": p99, "what": "e2e control step (host state/plan -> control)"},
+        "roofline": {
+            "bound": "fp32",
+            "kernel": "lwpr_kernel",
+            "achieved": achieved,
+            "peak": peak_tflops,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_tflops,
+            "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json)",
+            "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
+            "flops_per_launch": lwpr_flops,
+            "flops_per_field": flops_per_field,
+            "traffic": lwpr_traffic(args.config),
+        },
+        "stages_ms": stages,
+        "clocks": clk,
+        "gpu_launches": args.steps * (KERNELS_PER_ITER + 1),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(cfgd, args.cpu_sample, args.cpu_seconds)
+        cb.pop("step_times_s", None)
+        cb["cpu_model"] = cpu_model()
+        line["cpu_baseline"] = cb
+    return line
+
+
+def run_reference(args):
+    cfgd, desc = workload(args.config)
+    cb = cpu_reference(cfgd, args.cpu_sample, 0.0, max_steps=args.warmup + args.steps)
+    times = cb.pop("step_times_s")[args.warmup:] or [cb["ms_per_step"] / 1e3]
+    step = sum(times) / len(times)
+    k = min(args.cpu_sample, cfgd["K"])
+    value = k * cfgd["T"] / step
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": 0,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 + f64 (numpy)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {desc}", **cfgd, "iterations_per_step": 1},
+        "cpu_baseline": {**cb, "value": value, "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return 0
+    line = run_ours(args, rank, world, local)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,110 @@
+// common.cuh — shared types and host/device helpers of the PI²-RH engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "pi2rh.h"
+
+#define PI2_HD __host__ __device__ __forceinline__
+
+namespace pi2 {
+
+constexpr int kRolloutBlock = 128;  // threads (= rollouts) per attitude / rollout block
+constexpr int kLwprBlock = 128;     // threads per LWPR block
+constexpr int kLwprRows = 8;        // rows (k,t) per LWPR thread (register blocking)
+constexpr int kChunk = 256;         // rollouts per leaf partial (fixed => G-invariant tree)
+constexpr int kChunkWarps = 8;      // warps per partials block
+constexpr int kSeg = 1024;          // leaves per combine segment
+constexpr int kMaxSmallM = 8;       // sub-rollouts held in registers
+constexpr double kPi = 3.141592653589793;        // np.pi
+constexpr double kTwoPi = 6.283185307179586;     // 2.0 * math.pi
+constexpr double kLog2e = 1.4426950408889634;
+// LWPR weights are evaluated as 2^(logit*log2e + kExpShift): every weight the
+// reference can represent (float32 denormals included) is a
+// normal float here, so ex2.approx.ftz is exact-range.
+constexpr double kExpShift = 64.0;
+// below this (scaled) normaliser a row is re-evaluated with the reference's
+// denormal rounding emulated: unscaled den < 2^-110.
+constexpr float kSlowDen = 1.4210854715202004e-14f;  // 2^-46
+
+// float records per receptive field in HBM/shared memory
+constexpr int kRecDiag = 16;  // 4 x float4
+constexpr int kRecFull = 24;  // 6 x float4
+
+// Host/device exact arithmetic (no contraction) for code whose rounding must
+// match on both sides.
+#ifdef __CUDA_ARCH__
+#define PI2_DADD(a, b) __dadd_rn((a), (b))
+#define PI2_DSUB(a, b) __dsub_rn((a), (b))
+#define PI2_DMUL(a, b) __dmul_rn((a), (b))
+#define PI2_DDIV(a, b) __ddiv_rn((a), (b))
+#else
+#define PI2_DADD(a, b) ((a) + (b))
+#define PI2_DSUB(a, b) ((a) - (b))
+#define PI2_DMUL(a, b) ((a) * (b))
+#define PI2_DDIV(a, b) ((a) / (b))
+#endif
+
+// Per-call data read by the kernels from device memory (so that CUDA graph
+// replays pick up new state / keys / cost without re-capture).
+struct StepArgs {
+  double state[12];
+  uint64_t keys[PI2_MAX_ITERATIONS][2][2];  // [iteration][control|dynamics][k0,k1]
+  double std[4];
+  double neg_inv_temp;  // -1 / temperature (controller.py:368)
+  double ceiling;       // cost_ceiling (controller.py:243-246)
+  pi2_cost cost;
+};
+
+struct DynParams {
+  double dt, gain_dt;  // gain_dt = rate_gain * dt (controller.py:266)
+  double lo[4], hi[4];
+  float dt32, dt2_32;   // float32(dt), float32(dt)^2 (controller.py:255, :297)
+  float inv_m32, g32;   // AnalyticModel constants (dynamics.py:172-173)
+};
+
+struct AxisHeader {
+  float g0, gs[4];  // global linear shift g(x) = g0 + gs.x folded out of the local models
+  int num_fields;
+  int64_t offset;   // float offset of the axis' first record
+};
+
+// ---- path-integral partials: (min S, Z, V[4]) per timestep ---------------
+// Leaf: m = min_k S, Z = sum exp((S-m)*neg_inv), V = sum exp(..)*eps.
+// a <- a (+) b, fixed arithmetic; Z == 0 marks the identity.
+PI2_HD void partial_combine(double *a, const double *b, double neg_inv) {
+  if (b[1] == 0.0) return;
+  if (a[1] == 0.0) {
+    for (int i = 0; i < PI2_PARTIAL_WIDTH; ++i) a[i] = b[i];
+    return;
+  }
+  const double m = a[0] < b[0] ? a[0] : b[0];
+  const double sa = exp(PI2_DMUL(PI2_DSUB(a[0], m), neg_inv));
+  const double sb = exp(PI2_DMUL(PI2_DSUB(b[0], m), neg_inv));
+  a[0] = m;
+  for (int i = 1; i < PI2_PARTIAL_WIDTH; ++i)
+    a[i] = PI2_DADD(PI2_DMUL(a[i], sa), PI2_DMUL(b[i], sb));
+}
+
+// splitmix64 + the reference's stream-address chain (rng.py:24-44).
+PI2_HD uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline void derive_key(uint64_t seed, uint64_t stream, uint64_t cycle, uint64_t iteration,
+                       uint64_t out[2]) {
+  uint64_t h = splitmix64(seed);
+  h = splitmix64(h ^ stream);
+  h = splitmix64(h ^ cycle);
+  h = splitmix64(h ^ iteration);
+  out[0] = splitmix64(h);
+  out[1] = splitmix64(h ^ 0xA5A5A5A5A5A5A5A5ull);
+}
+
+}  // namespace pi2

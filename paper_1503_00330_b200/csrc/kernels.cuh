@@ -1,0 +1,657 @@
+// kernels.cuh — sm_100a kernels of one PI²-RH optimisation iteration.
+//
+//   attitude_kernel  K1-K3: perturb + clip, FP64 attitude recurrence, LWPR rows
+//   lwpr_kernel      K4:    batched LWPR predict (FP32 CUDA cores + MUFU ex2)
+//   rollout_kernel   K5-K10: sub-rollout integration, cost, M-mean, suffix sum
+//   partials_kernel  K11a:  per-chunk (min, Z, V) softmax partials
+//   combine_kernel   K11b:  fixed-order tree combine + plan update
+//
+// Row (k, t) of a rollout batch is index k * N + t everywhere (the
+// reference's xin layout, controller.py:272-275).
+#pragma once
+
+#include "common.cuh"
+
+namespace pi2 {
+
+// ---------------------------------------------------------------------------
+// device noise: Philox4x32-10 + Box-Muller, keyed by the reference's stream
+// address (rng.py:33-44); counter = element-group index + key word 1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
+  const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);  // (0,1]
+  const float u2 = (float)b * 2.3283064365386963e-10f;                                   // [0,1)
+  const float r = sqrtf(-2.0f * logf(u1));
+  float s, c;
+  sincospif(2.0f * u2, &s, &c);
+  return make_float2(r * c, r * s);
+}
+
+__device__ __forceinline__ float4 normals4(uint64_t index, uint64_t k0, uint64_t k1) {
+  const uint4 c = make_uint4((uint32_t)index, (uint32_t)(index >> 32), (uint32_t)k1,
+                             (uint32_t)(k1 >> 32));
+  const uint4 r = philox4x32_10(c, (uint32_t)k0, (uint32_t)(k0 >> 32));
+  const float2 z0 = box_muller(r.x, r.y), z1 = box_muller(r.z, r.w);
+  return make_float4(z0.x, z0.y, z1.x, z1.y);
+}
+
+// exploration noise eps[k, t, :] of the device stream (float32 normals x float64 std)
+__device__ __forceinline__ void device_eps(const StepArgs *sa, int it, uint64_t kg, int N, int t,
+                                           double e[4]) {
+  const float4 z = normals4(kg * (uint64_t)N + (uint64_t)t, sa->keys[it][0][0], sa->keys[it][0][1]);
+  e[0] = __dmul_rn((double)z.x, sa->std[0]);
+  e[1] = __dmul_rn((double)z.y, sa->std[1]);
+  e[2] = __dmul_rn((double)z.z, sa->std[2]);
+  e[3] = __dmul_rn((double)z.w, sa->std[3]);
+}
+
+// wrap_angle: pi - mod(pi - a, 2 pi) with numpy float remainder semantics
+// (dynamics.py:27-29; npy_divmod: fmod, then shift into the divisor's sign).
+__device__ __forceinline__ double wrap_angle(double a) {
+  const double x = __dsub_rn(kPi, a);
+  double m = fmod(x, kTwoPi);
+  if (m != 0.0) {
+    if (m < 0.0) m = __dadd_rn(m, kTwoPi);
+  } else {
+    m = 0.0;
+  }
+  return __dsub_rn(kPi, m);
+}
+
+// ---------------------------------------------------------------------------
+// K1-K3: u = clip(plan + eps), attitude recurrence, LWPR input rows.
+// controller.py:257-275.  One thread per rollout, FP64, no contraction.
+// ---------------------------------------------------------------------------
+template <bool DEVICE_NOISE>
+__global__ void __launch_bounds__(kRolloutBlock)
+    attitude_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
+                    const double *__restrict__ eps, int iteration, int64_t K, int64_t k_off, int N,
+                    DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last,
+                    double *__restrict__ eps_out) {
+  extern __shared__ double splan[];  // (N, 4)
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) splan[i] = plan[i];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double ang[3] = {sa->state[6], sa->state[7], sa->state[8]};
+  double rate[3] = {sa->state[9], sa->state[10], sa->state[11]};
+  const double *ek = DEVICE_NOISE ? nullptr : eps + k * (int64_t)N * 4;
+  float4 *xk = xin + k * (int64_t)N;
+  for (int t = 0; t < N; ++t) {
+    double e[4];
+    if (DEVICE_NOISE) {
+      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+      if (eps_out) {
+        double2 *o = reinterpret_cast<double2 *>(eps_out + (k * (int64_t)N + t) * 4);
+        o[0] = make_double2(e[0], e[1]);
+        o[1] = make_double2(e[2], e[3]);
+      }
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
+      e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    }
+    double u[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      u[c] = fmin(fmax(__dadd_rn(splan[4 * t + c], e[c]), dp.lo[c]), dp.hi[c]);
+    xk[t] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
+                        __double2float_rn(ang[2]), __double2float_rn(u[3]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      ang[c] = wrap_angle(__dadd_rn(ang[c], __dmul_rn(rate[c], dp.dt)));
+      rate[c] = __dadd_rn(rate[c], __dmul_rn(dp.gain_dt, __dsub_rn(u[c], rate[c])));
+    }
+  }
+  ang_last[k] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
+                            __double2float_rn(ang[2]), 0.0f);
+}
+
+// ---------------------------------------------------------------------------
+// K4: batched LWPR predict.  Weights 2^(logit2) with logit2 = Horner form of
+// the folded quadratic (log2-scaled, +kExpShift); local models shifted by a
+// global linear g(x) so the one-pass second moment does not cancel.
+// Thread = kLwprRows rows; all threads of a block walk the same receptive
+// field at the same time (shared-memory broadcast of the field record).
+// ---------------------------------------------------------------------------
+struct LwprArgs {
+  const float *params;  // records of all axes (HBM)
+  AxisHeader axis[3];
+  int a_begin, a_end;
+  int full;             // record layout kRecFull (else kRecDiag)
+  int resident;         // all records of [a_begin, a_end) fit in shared memory
+  int tile;             // fields per shared-memory tile when not resident
+  int64_t rows;
+  const float4 *x;      // (rows) inputs, padded to 4
+  float *mean_out;      // [row * out_stride + axis - a_begin]
+  float *sd_out;        // std (sqrt_out) or variance; may be null
+  int out_stride;
+  int sqrt_out;
+};
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <bool FULL>
+__device__ __forceinline__ float field_logit2(const float *f, const float4 &x) {
+  if (!FULL) {
+    // f: A0, A1[4], A2[4], S[4], Y0, LV, -
+    float lg = fmaf(fmaf(f[1], x.x, f[5]), x.x, f[0]);
+    lg = fmaf(fmaf(f[2], x.y, f[6]), x.y, lg);
+    lg = fmaf(fmaf(f[3], x.z, f[7]), x.z, lg);
+    return fmaf(fmaf(f[4], x.w, f[8]), x.w, lg);
+  } else {
+    // f: A0, Q00 Q01 Q02 Q03, Q11 Q12 Q13, Q22 Q23, Q33, A2[4], S[4], Y0, LV
+    float h = fmaf(f[1], x.x, f[11]);
+    h = fmaf(f[2], x.y, h);
+    h = fmaf(f[3], x.z, h);
+    h = fmaf(f[4], x.w, h);
+    float lg = fmaf(h, x.x, f[0]);
+    h = fmaf(f[5], x.y, f[12]);
+    h = fmaf(f[6], x.z, h);
+    h = fmaf(f[7], x.w, h);
+    lg = fmaf(h, x.y, lg);
+    h = fmaf(f[8], x.z, f[13]);
+    h = fmaf(f[9], x.w, h);
+    lg = fmaf(h, x.z, lg);
+    h = fmaf(f[10], x.w, f[14]);
+    return fmaf(h, x.w, lg);
+  }
+}
+
+template <bool FULL>
+__device__ __forceinline__ float field_local(const float *f, const float4 &x) {
+  constexpr int S = FULL ? 15 : 9;
+  float y = fmaf(f[S + 0], x.x, f[S + 4]);
+  y = fmaf(f[S + 1], x.y, y);
+  y = fmaf(f[S + 2], x.z, y);
+  return fmaf(f[S + 3], x.w, y);
+}
+
+template <bool FULL>
+__device__ __forceinline__ float field_lvar(const float *f) {
+  return f[FULL ? 20 : 14];
+}
+
+// Reference-exact evaluation of one row (rare: every weight is (nearly)
+// denormal in float32).  Emulates numpy: e = expf(q) with float32 denormal
+// rounding (here scaled by 2^64: multiples of 2^-85 below 2^-62), w = e/den
+// (0/0 = NaN -> cost ceiling downstream), mean = sum w y, two-pass variance
+// (lwpr.py:395-407).
+template <bool FULL>
+__device__ __forceinline__ float exact_weight(const float *f, const float4 &x) {
+  float e = exp2f(field_logit2<FULL>(f, x));  // IEEE exp2f: never flushes
+  // float32 denormal grid of exp(q) (step 2^-149), in 2^64-scaled units:
+  // multiples of 2^-85 below 2^-62 (exact products by powers of two)
+  if (e < 2.168404344971009e-19f) e = rintf(e * 3.8685626227668134e25f) * 2.5849394142282115e-26f;
+  return e;
+}
+
+template <bool FULL>
+__device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, float gx,
+                                            float *mean_out, float *var_out) {
+  constexpr int RS = FULL ? kRecFull : kRecDiag;
+  float den = 0.0f;
+  for (int l = 0; l < nf; ++l) den = __fadd_rn(den, exact_weight<FULL>(rec + (int64_t)l * RS, x));
+  float mean = 0.0f;
+  for (int l = 0; l < nf; ++l) {
+    const float *f = rec + (int64_t)l * RS;
+    const float w = __fdiv_rn(exact_weight<FULL>(f, x), den);
+    mean = __fadd_rn(mean, __fmul_rn(w, __fadd_rn(field_local<FULL>(f, x), gx)));
+  }
+  float var = 0.0f;
+  for (int l = 0; l < nf; ++l) {
+    const float *f = rec + (int64_t)l * RS;
+    const float w = __fdiv_rn(exact_weight<FULL>(f, x), den);
+    const float d = __fsub_rn(mean, __fadd_rn(field_local<FULL>(f, x), gx));
+    var = __fadd_rn(var, __fmul_rn(w, __fadd_rn(__fmul_rn(d, d), field_lvar<FULL>(f))));
+  }
+  *mean_out = mean;
+  *var_out = var;
+}
+
+template <bool FULL, bool VAR, int R>
+__global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
+  constexpr int RS = FULL ? kRecFull : kRecDiag;
+  extern __shared__ float4 smem4[];
+  float *srec = reinterpret_cast<float *>(smem4);
+
+  const int64_t row0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R;
+  float4 x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t row = row0 + r < a.rows ? row0 + r : a.rows - 1;
+    x[r] = __ldg(a.x + row);
+  }
+
+  if (a.resident) {
+    const int64_t base = a.axis[a.a_begin].offset;
+    const int64_t n4 = (a.axis[a.a_end - 1].offset + (int64_t)a.axis[a.a_end - 1].num_fields * RS - base) / 4;
+    const float4 *src = reinterpret_cast<const float4 *>(a.params + base);
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) smem4[i] = __ldg(src + i);
+    __syncthreads();
+  }
+
+  for (int ax = a.a_begin; ax < a.a_end; ++ax) {
+    const AxisHeader h = a.axis[ax];
+    float den[R], num[R], m2[R], lv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) den[r] = num[r] = m2[r] = lv[r] = 0.0f;
+
+    const int tile = a.resident ? h.num_fields : a.tile;
+    for (int l0 = 0; l0 < h.num_fields; l0 += tile) {
+      const int nl = min(tile, h.num_fields - l0);
+      const float *sp;
+      if (a.resident) {
+        sp = srec + (h.offset - a.axis[a.a_begin].offset) + (int64_t)l0 * RS;
+      } else {
+        __syncthreads();
+        const float4 *src = reinterpret_cast<const float4 *>(a.params + h.offset + (int64_t)l0 * RS);
+        for (int i = threadIdx.x; i < nl * RS / 4; i += blockDim.x) smem4[i] = __ldg(src + i);
+        __syncthreads();
+        sp = srec;
+      }
+#pragma unroll 1
+      for (int l = 0; l < nl; ++l) {
+        float f[RS];
+#pragma unroll
+        for (int i = 0; i < RS / 4; ++i) {
+          const float4 v = reinterpret_cast<const float4 *>(sp + (int64_t)l * RS)[i];
+          f[4 * i + 0] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float e = ex2_ftz(field_logit2<FULL>(f, x[r]));
+          const float y = field_local<FULL>(f, x[r]);
+          den[r] += e;
+          if (VAR) {
+            const float ey = e * y;
+            num[r] += ey;
+            m2[r] = fmaf(ey, y, m2[r]);
+            lv[r] = fmaf(e, field_lvar<FULL>(f), lv[r]);
+          } else {
+            num[r] = fmaf(e, y, num[r]);
+          }
+        }
+      }
+    }
+
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = row0 + r;
+      if (row >= a.rows) continue;
+      const float gx = fmaf(h.gs[3], x[r].w, fmaf(h.gs[2], x[r].z, fmaf(h.gs[1], x[r].y, fmaf(h.gs[0], x[r].x, h.g0))));
+      float mean, var = 0.0f;
+      if (den[r] >= kSlowDen) {
+        const float mp = __fdiv_rn(num[r], den[r]);
+        mean = __fadd_rn(gx, mp);
+        if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(m2[r], lv[r]), den[r]), __fmul_rn(mp, mp)), 0.0f);
+      } else {
+        lwpr_row_exact<FULL>(a.params + h.offset, h.num_fields, x[r], gx, &mean, &var);
+      }
+      const int64_t o = row * a.out_stride + (ax - a.a_begin);
+      a.mean_out[o] = mean;
+      if (VAR && a.sd_out) a.sd_out[o] = a.sqrt_out ? __fsqrt_rn(var) : var;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5-K10: sub-rollout integration, crash, stage cost, pairwise M-mean,
+// float64 suffix sum, non-finite -> ceiling.  controller.py:281-322,
+// simworld.py:157-198.  One thread per rollout; FP32 without contraction so
+// pos/vel match the reference's cumsum form bitwise given the same accels.
+// ---------------------------------------------------------------------------
+struct RollArgs {
+  const StepArgs *sa;
+  int iteration;
+  int64_t K, k_off;
+  int N, M;
+  int model;        // PI2_MODEL_*
+  int spread;       // model.probabilistic && M > 1
+  int device_dyn;   // dynamics draws from the device stream (else dyn)
+  float two_point;  // TwoPointModel magnitude
+  DynParams dp;
+  const float4 *xin, *ang_last;
+  const float4 *lw_mean, *lw_std;
+  const float *dyn;  // (K, M, N, 3)
+  double *costs;     // (K, N)
+  uint8_t *crash;    // (K)
+};
+
+__device__ __forceinline__ float sign_of(float v) {  // np.sign (0 -> 0, NaN -> NaN)
+  return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : v);
+}
+
+__device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, float py, float pz,
+                                                float vx, float vy, float vz, float angterm,
+                                                bool crashed) {
+  float d = __fsub_rn(px, c.waypoint[0]);
+  float out = __fmul_rn(d, d);
+  d = __fsub_rn(py, c.waypoint[1]);
+  out = __fadd_rn(out, __fmul_rn(d, d));
+  d = __fsub_rn(pz, c.waypoint[2]);
+  out = __fadd_rn(out, __fmul_rn(__fmul_rn(d, d), 10.0f));
+  float t = __fmul_rn(vx, vx);
+  t = __fadd_rn(t, __fmul_rn(vy, vy));
+  t = __fadd_rn(t, __fmul_rn(vz, vz));
+  out = __fadd_rn(out, __fmul_rn(t, 0.1f));
+  out = __fadd_rn(out, angterm);
+  for (int i = 0; i < c.n_obstacles; ++i) {
+    float dx = __fsub_rn(px, c.obstacles[2 * i]);
+    float dy = __fsub_rn(py, c.obstacles[2 * i + 1]);
+    t = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    t = __fmul_rn(expf(__fmul_rn(t, -10.0f)), 100.0f);
+    out = __fadd_rn(out, t);
+  }
+  return __fadd_rn(out, crashed ? 10.0f : 0.0f);
+}
+
+template <int MM>  // compile-time M (1..kMaxSmallM), or 0 = runtime M <= PI2_MAX_SUB_ROLLOUTS
+__global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
+  constexpr int MCAP = MM > 0 ? MM : PI2_MAX_SUB_ROLLOUTS;
+  extern __shared__ float sq[];  // (N, blockDim): this thread's stage costs, column tid
+  __shared__ pi2_cost cost;
+  if (threadIdx.x == 0) cost = a.sa->cost;
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.K) return;
+  const int M = MM > 0 ? MM : a.M;
+  const int N = a.N;
+  const int S = a.spread ? M : 1;
+  const StepArgs *sa = a.sa;
+  const float p0[3] = {__double2float_rn(sa->state[0]), __double2float_rn(sa->state[1]),
+                       __double2float_rn(sa->state[2])};
+  const float v0[3] = {__double2float_rn(sa->state[3]), __double2float_rn(sa->state[4]),
+                       __double2float_rn(sa->state[5])};
+  const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
+  const uint64_t kg = (uint64_t)(a.k_off + k);
+  const bool threshold_cost = cost.kind == PI2_COST_THRESHOLD;
+
+  float cs[MCAP][3], ccs[MCAP][3];
+  bool crashed[MCAP];
+#pragma unroll
+  for (int m = 0; m < MCAP; ++m) {
+    crashed[m] = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cs[m][c] = ccs[m][c] = -0.0f;  // -0 + x == x: cumsum start
+  }
+
+  for (int t = 0; t < N; ++t) {
+    const int64_t row = k * (int64_t)N + t;
+    float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
+    if (a.model == PI2_MODEL_HYBRID_LWPR) {
+      const float4 m4 = a.lw_mean[row];
+      mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
+      if (a.spread) {
+        const float4 s4 = a.lw_std[row];
+        sd[0] = s4.x; sd[1] = s4.y; sd[2] = s4.z;
+      }
+    } else if (a.model == PI2_MODEL_ANALYTIC) {  // dynamics.py:175-185
+      const float4 xr = a.xin[row];
+      float sr, cr, sp, cp, sy, cy;
+      sincosf(xr.x, &sr, &cr);
+      sincosf(xr.y, &sp, &cp);
+      sincosf(xr.z, &sy, &cy);
+      const float fm = __fmul_rn(xr.w, a.dp.inv_m32);
+      const float crsp = __fmul_rn(cr, sp);
+      mn[0] = __fmul_rn(fm, __fadd_rn(__fmul_rn(crsp, cy), __fmul_rn(sr, sy)));
+      mn[1] = __fmul_rn(fm, __fsub_rn(__fmul_rn(crsp, sy), __fmul_rn(sr, cy)));
+      mn[2] = __fsub_rn(__fmul_rn(fm, __fmul_rn(cr, cp)), a.dp.g32);
+    } else {  // two-point test model (tests/synthetic.py:402-411)
+      mn[0] = mn[1] = mn[2] = 0.0f;
+      sd[2] = a.two_point;
+    }
+    const float4 ap = (t + 1 < N) ? a.xin[row + 1] : a.ang_last[k];  // post-step attitude
+    const float angterm = __fmul_rn(
+        __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
+    const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
+    float q[MCAP];
+#pragma unroll
+    for (int m = 0; m < MCAP; ++m) {
+      if (m >= S) break;
+      float acc[3];
+      if (a.spread) {
+        float d[3];
+        if (a.device_dyn) {
+          const float4 z = normals4((kg * (uint64_t)M + (uint64_t)m) * (uint64_t)N + (uint64_t)t, dk0, dk1);
+          d[0] = z.x; d[1] = z.y; d[2] = z.z;
+        } else {
+          const float *dp = a.dyn + ((k * M + m) * (int64_t)N + t) * 3;
+          d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
+        }
+        if (a.model == PI2_MODEL_TWO_POINT) {
+          d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = __fadd_rn(__fmul_rn(sd[c], d[c]), mn[c]);
+      } else {
+        acc[0] = mn[0]; acc[1] = mn[1]; acc[2] = mn[2];
+      }
+      float pos[3], vel[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        cs[m][c] = __fadd_rn(cs[m][c], acc[c]);
+        ccs[m][c] = __fadd_rn(ccs[m][c], cs[m][c]);
+        vel[c] = __fadd_rn(__fmul_rn(cs[m][c], a.dp.dt32), v0[c]);
+        pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[m][c], cs[m][c]), a.dp.dt2_32),
+                                     __fmul_rn(sdt, v0[c])),
+                           p0[c]);
+      }
+      if (threshold_cost) {
+        q[m] = pos[2] > cost.threshold ? 1.0f : 0.0f;
+      } else {
+        crashed[m] = crashed[m] || (pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
+                     (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) ||
+                     (pos[1] > cost.arena_hi[1]) || (pos[2] > cost.arena_hi[2]);
+        q[m] = nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[m]);
+      }
+    }
+    // sub-rollout mean: pairwise halving while even, plain mean when odd
+    // (controller.py:314-319)
+    int n = S;
+    while (n > 1) {
+      if ((n & 1) == 0) {
+#pragma unroll
+        for (int i = 0; i < MCAP / 2; ++i)
+          if (i < n / 2) q[i] = __fmul_rn(0.5f, __fadd_rn(q[2 * i], q[2 * i + 1]));
+        n >>= 1;
+      } else {
+        float s = q[0];
+#pragma unroll
+        for (int i = 1; i < MCAP; ++i)
+          if (i < n) s = __fadd_rn(s, q[i]);
+        q[0] = __fdiv_rn(s, (float)n);
+        n = 1;
+      }
+    }
+    sq[t * blockDim.x + threadIdx.x] = q[0];
+  }
+
+  bool crash = false;
+#pragma unroll
+  for (int m = 0; m < MCAP; ++m)
+    if (m < S) crash = crash || crashed[m];
+  // float64 suffix sum (controller.py:320-322) and ceiling (:243-246)
+  const double dt = a.dp.dt, ceiling = sa->ceiling;
+  double acc = 0.0;
+  double *out = a.costs + k * (int64_t)N;
+  for (int t = N - 1; t >= 0; --t) {
+    const double s = __dmul_rn((double)sq[t * blockDim.x + threadIdx.x], dt);
+    acc = (t == N - 1) ? s : __dadd_rn(acc, s);
+    double v = acc;
+    if (!isfinite(v)) {
+      v = ceiling;
+      crash = true;
+    }
+    out[t] = v;
+  }
+  a.crash[k] = crash ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// K11a: leaf partials of the per-timestep softmax (controller.py:367-370):
+// per chunk of kChunk rollouts and per t: m = min S, Z = sum w, V = sum w eps,
+// w = exp((S - m) * neg_inv).  Warp w handles t = w, w + 8, ...; lane order and
+// the xor butterfly are fixed, lane 0's value is kept: deterministic.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(32 * kChunkWarps)
+    partials_kernel(const double *__restrict__ costs, const double *__restrict__ eps,
+                    const StepArgs *__restrict__ sa, int iteration, int64_t K, int64_t k_off, int N,
+                    double neg_inv, double *__restrict__ out) {
+  constexpr int J = kChunk / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * kChunk;
+  for (int t = warp; t < N; t += kChunkWarps) {
+    double s[J];
+    double m = INFINITY;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = k0 + lane + 32 * j;
+      s[j] = k < K ? costs[k * N + t] : INFINITY;
+      m = fmin(m, s[j]);
+    }
+    m = warp_min(m);
+    double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t k = k0 + lane + 32 * j;
+      if (k >= K) continue;
+      const double w = exp(__dmul_rn(__dsub_rn(s[j], m), neg_inv));
+      double e[4];
+      if (eps) {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
+        const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
+        e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+      } else {
+        device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+      }
+      z = __dadd_rn(z, w);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __dadd_rn(v[c], __dmul_rn(w, e[c]));
+    }
+    z = warp_sum(z);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = warp_sum(v[c]);
+    if (lane == 0) {
+      double *o = out + ((int64_t)blockIdx.x * N + t) * PI2_PARTIAL_WIDTH;
+      o[0] = m; o[1] = z; o[2] = v[0]; o[3] = v[1]; o[4] = v[2]; o[5] = v[3];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K11b: per-timestep adjacent binary tree over `n` partials laid out
+// (n, N, 6): segments of kSeg leaves reduced in shared memory, then the
+// segment roots.  Identical tree for any split of the leaves into aligned
+// power-of-two runs (one per GPU) => G-invariant update.  Optionally writes
+// the root and/or applies plan[t] = clip(plan[t] + V/Z) (controller.py:369-371).
+// ---------------------------------------------------------------------------
+__device__ void smem_tree(double (*v)[PI2_PARTIAL_WIDTH], int n, double neg_inv) {
+  for (int st = 1; st < n; st <<= 1) {
+    const int pairs = (n + 2 * st - 1) / (2 * st);
+    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+      const int i = p * 2 * st;
+      if (i + st < n) partial_combine(v[i], v[i + st], neg_inv);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    combine_kernel(const double *__restrict__ leaves, int64_t n, int N, double neg_inv,
+                   double *__restrict__ root_out, double *__restrict__ plan, DynParams dp) {
+  extern __shared__ double cmb[];
+  double(*seg)[PI2_PARTIAL_WIDTH] = reinterpret_cast<double(*)[PI2_PARTIAL_WIDTH]>(cmb);
+  double(*roots)[PI2_PARTIAL_WIDTH] = seg + kSeg;
+  const int t = blockIdx.x;
+  const int64_t nseg = (n + kSeg - 1) / kSeg;
+  for (int64_t s = 0; s < nseg; ++s) {
+    const int cnt = (int)(n - s * kSeg < kSeg ? n - s * kSeg : kSeg);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double *src = leaves + ((s * kSeg + i) * N + t) * PI2_PARTIAL_WIDTH;
+#pragma unroll
+      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) seg[i][c] = src[c];
+    }
+    __syncthreads();
+    smem_tree(seg, cnt, neg_inv);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) roots[s][c] = seg[0][c];
+    }
+    __syncthreads();
+  }
+  smem_tree(roots, (int)nseg, neg_inv);
+  if (threadIdx.x == 0) {
+    if (root_out) {
+#pragma unroll
+      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) root_out[t * PI2_PARTIAL_WIDTH + c] = roots[0][c];
+    }
+    if (plan) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double du = __ddiv_rn(roots[0][2 + c], roots[0][1]);
+        plan[4 * t + c] = fmin(fmax(__dadd_rn(plan[4 * t + c], du), dp.lo[c]), dp.hi[c]);
+      }
+    }
+  }
+}
+
+// plan <- shifted plan (ControlPlan.shifted, controller.py:63-66), on device
+__global__ void shift_plan_kernel(const double *__restrict__ src, double *__restrict__ dst, int N) {
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) {
+    const int t = i / 4, c = i % 4;
+    dst[i] = src[4 * (t + 1 < N ? t + 1 : N - 1) + c];
+  }
+}
+
+// device noise materialisation (tests / RolloutBatch.noise of device mode)
+__global__ void noise_kernel(const StepArgs *__restrict__ sa, int which, int iteration, int64_t K,
+                             int64_t k_off, int N, int M, double *__restrict__ eps_out,
+                             float *__restrict__ dyn_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (which == PI2_STREAM_CONTROL) {
+    if (i >= K * N) return;
+    const int64_t k = i / N;
+    const int t = (int)(i % N);
+    double e[4];
+    device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) eps_out[i * 4 + c] = e[c];
+  } else {
+    if (i >= K * M * N) return;  // i = (k * M + m) * N + t
+    const uint64_t kg_idx = (uint64_t)(k_off * M * N + i);
+    const float4 z = normals4(kg_idx, sa->keys[iteration][1][0], sa->keys[iteration][1][1]);
+    dyn_out[i * 3 + 0] = z.x;
+    dyn_out[i * 3 + 1] = z.y;
+    dyn_out[i * 3 + 2] = z.z;
+  }
+}
+
+}  // namespace pi2

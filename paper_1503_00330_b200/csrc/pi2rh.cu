@@ -1,0 +1,963 @@
+// pi2rh.cu — C ABI of the B200 PI²-RH engine (declared in include/pi2rh.h).
+//
+// One context = one RolloutEngine (controller.py:161-247) bound to one GPU:
+// it owns the HBM workspaces of its K x N batch, the staged model / cost
+// plugins, pinned staging memory and a cached CUDA graph of a whole control
+// step.  Host compute here is limited to parameter folding (FrozenLwpr's
+// constructor, lwpr.py:339-358) and stream-key hashing (rng.py:33-44).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace pi2;
+
+struct AxisRaw {
+  int L = 0, d = 0;
+  std::vector<double> centers, metrics, coefs, lvar;
+};
+
+struct pi2_ctx {
+  int device = 0;
+  pi2_dims dims{};
+  int64_t K = 0;
+  int N = 0, M = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t staged = nullptr;  // last H2D from the pinned staging block
+  std::string err;
+
+  // plugins
+  bool have_dyn = false;
+  pi2_dynamics dyn{};
+  DynParams dp{};
+  bool have_cost = false;
+  pi2_cost cost{};
+  int model = PI2_MODEL_NONE;
+  double model_param = 0.0;
+  AxisRaw axes[3];
+  bool params_dirty = true;
+  bool params_full = false;
+  AxisHeader hdr[3]{};
+  float *d_params = nullptr;
+  size_t params_cap = 0;
+
+  // device workspaces (sized by dims)
+  StepArgs *d_args = nullptr;
+  double *d_plan = nullptr, *d_plan2 = nullptr;
+  float4 *d_xin = nullptr, *d_ang_last = nullptr, *d_lw = nullptr;  // d_lw: mean rows then std rows
+  double *d_costs = nullptr;
+  uint8_t *d_crash = nullptr;
+  double *d_partials = nullptr, *d_root = nullptr;
+  int64_t n_chunks = 0;
+  // lazily grown scratch
+  double *d_noise = nullptr;
+  size_t noise_cap = 0;
+  float *d_dynbuf = nullptr;
+  size_t dyn_cap = 0;
+  void *d_scratch = nullptr;
+  size_t scratch_cap = 0;
+
+  // pinned staging
+  StepArgs *h_args = nullptr;
+  double *h_plan = nullptr;  // N x 4
+
+  // graph cache for pi2_optimize
+  cudaGraphExec_t graph = nullptr;
+  int graph_iters = -1;
+  double graph_neg_inv = 0.0;
+
+  int smem_optin = 0;
+};
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+int fail(pi2_ctx *ctx, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf; else g_noctx_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? PI2_ERR_OOM : PI2_ERR_CUDA,          \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);       \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int rc_ = (expr);        \
+    if (rc_ != PI2_OK) return rc_; \
+  } while (0)
+
+cudaStream_t pick(pi2_ctx *ctx, void *s) { return s ? (cudaStream_t)s : ctx->stream; }
+
+int ensure(pi2_ctx *ctx, void **p, size_t *cap, size_t bytes) {
+  if (*cap >= bytes && *p) return PI2_OK;
+  if (*p) CU(cudaFree(*p));
+  *p = nullptr;
+  *cap = 0;
+  CU(cudaMalloc(p, std::max<size_t>(bytes, 256)));
+  *cap = bytes;
+  return PI2_OK;
+}
+
+int bind(pi2_ctx *ctx) {
+  CU(cudaSetDevice(ctx->device));
+  return PI2_OK;
+}
+
+void invalidate_graph(pi2_ctx *ctx) {
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  ctx->graph = nullptr;
+  ctx->graph_iters = -1;
+}
+
+// ---- FrozenLwpr folding (lwpr.py:339-358), float64, padded to 4 inputs ----
+bool axis_is_diagonal(const AxisRaw &a) {
+  for (int l = 0; l < a.L; ++l)
+    for (int i = 0; i < a.d; ++i)
+      for (int j = 0; j < a.d; ++j)
+        if (i != j && a.metrics[((size_t)l * a.d + i) * a.d + j] != 0.0) return false;
+  return true;
+}
+
+void fold_axis(const AxisRaw &a, bool full, std::vector<float> &rec, AxisHeader &h) {
+  const int RS = full ? kRecFull : kRecDiag;
+  const size_t base = rec.size();
+  rec.resize(base + (size_t)a.L * RS, 0.0f);
+  std::vector<double> y0(a.L), s(4 * (size_t)a.L, 0.0);
+  double g0 = 0.0, gs[4] = {0, 0, 0, 0};
+  for (int l = 0; l < a.L; ++l) {
+    double yy = a.coefs[(size_t)l * (a.d + 1)];
+    for (int i = 0; i < a.d; ++i) {
+      const double si = a.coefs[(size_t)l * (a.d + 1) + 1 + i];
+      s[4 * (size_t)l + i] = si;
+      yy -= si * a.centers[(size_t)l * a.d + i];  // y0 = coef0 - s.c (lwpr.py:355-357)
+    }
+    y0[l] = yy;
+    g0 += yy;
+    for (int i = 0; i < 4; ++i) gs[i] += s[4 * (size_t)l + i];
+  }
+  g0 /= a.L;
+  for (double &v : gs) v /= a.L;
+  h.g0 = (float)g0;
+  for (int i = 0; i < 4; ++i) h.gs[i] = (float)gs[i];
+  h.num_fields = a.L;
+  h.offset = (int64_t)base;
+  for (int l = 0; l < a.L; ++l) {
+    double c[4] = {0, 0, 0, 0}, D[4][4] = {{0}};
+    for (int i = 0; i < a.d; ++i) {
+      c[i] = a.centers[(size_t)l * a.d + i];
+      for (int j = 0; j < a.d; ++j) D[i][j] = a.metrics[((size_t)l * a.d + i) * a.d + j];
+    }
+    double dc[4], a0 = 0.0;
+    for (int i = 0; i < 4; ++i) {  // dc = D c (lwpr.py:344)
+      dc[i] = 0.0;
+      for (int j = 0; j < 4; ++j) dc[i] += D[i][j] * c[j];
+    }
+    for (int i = 0; i < 4; ++i) a0 += dc[i] * c[i];
+    a0 *= -0.5;  // lwpr.py:347
+    float *f = rec.data() + base + (size_t)l * RS;
+    f[0] = (float)(a0 * kLog2e + kExpShift);
+    if (!full) {
+      for (int i = 0; i < 4; ++i) {
+        f[1 + i] = (float)(-0.5 * D[i][i] * kLog2e);  // a1 (lwpr.py:345)
+        f[5 + i] = (float)(dc[i] * kLog2e);           // a2 (lwpr.py:346)
+        f[9 + i] = (float)(s[4 * (size_t)l + i] - gs[i]);
+      }
+      f[13] = (float)(y0[l] - g0);
+      f[14] = (float)a.lvar[l];
+    } else {
+      int q = 1;
+      for (int i = 0; i < 4; ++i)
+        for (int j = i; j < 4; ++j)
+          f[q++] = (float)((i == j ? -0.5 * D[i][i] : -0.5 * (D[i][j] + D[j][i])) * kLog2e);
+      for (int i = 0; i < 4; ++i) {
+        f[11 + i] = (float)(dc[i] * kLog2e);
+        f[15 + i] = (float)(s[4 * (size_t)l + i] - gs[i]);
+      }
+      f[19] = (float)(y0[l] - g0);
+      f[20] = (float)a.lvar[l];
+    }
+  }
+}
+
+int ensure_params(pi2_ctx *ctx) {
+  if (!ctx->params_dirty) return PI2_OK;
+  bool full = false;
+  for (auto &a : ctx->axes)
+    if (a.L > 0 && !axis_is_diagonal(a)) full = true;
+  std::vector<float> rec;
+  for (int ax = 0; ax < 3; ++ax) {
+    if (ctx->axes[ax].L > 0) fold_axis(ctx->axes[ax], full, rec, ctx->hdr[ax]);
+    else ctx->hdr[ax] = AxisHeader{};
+  }
+  if (!rec.empty()) {
+    TRY(ensure(ctx, (void **)&ctx->d_params, &ctx->params_cap, rec.size() * sizeof(float)));
+    CU(cudaMemcpy(ctx->d_params, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  ctx->params_full = full;
+  ctx->params_dirty = false;
+  return PI2_OK;
+}
+
+// ---- kernel attribute setup -------------------------------------------------
+template <typename F>
+int set_smem(pi2_ctx *ctx, F *fn, int bytes) {
+  CU(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return PI2_OK;
+}
+
+int lwpr_smem_limit(pi2_ctx *ctx) { return std::min(ctx->smem_optin, 64 * 1024); }
+
+template <bool FULL, bool VAR, int R>
+int launch_lwpr_t(pi2_ctx *ctx, const LwprArgs &a, int smem, cudaStream_t st) {
+  auto *fn = lwpr_kernel<FULL, VAR, R>;
+  TRY(set_smem(ctx, fn, smem));
+  const int64_t per_block = (int64_t)kLwprBlock * R;
+  const int64_t grid = (a.rows + per_block - 1) / per_block;
+  fn<<<(unsigned)grid, kLwprBlock, smem, st>>>(a);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
+int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
+                float *sd_out, int stride, int sqrt_out, cudaStream_t st) {
+  TRY(ensure_params(ctx));
+  LwprArgs a{};
+  a.params = ctx->d_params;
+  for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
+  a.a_begin = a_begin;
+  a.a_end = a_end;
+  a.full = ctx->params_full;
+  const int RS = ctx->params_full ? kRecFull : kRecDiag;
+  int64_t fields = 0, maxL = 0;
+  for (int ax = a_begin; ax < a_end; ++ax) {
+    fields += ctx->hdr[ax].num_fields;
+    maxL = std::max<int64_t>(maxL, ctx->hdr[ax].num_fields);
+  }
+  const int limit = lwpr_smem_limit(ctx);
+  const int64_t need = fields * RS * (int64_t)sizeof(float);
+  int smem;
+  if (need <= limit) {
+    a.resident = 1;
+    a.tile = 0;
+    smem = (int)need;
+  } else {
+    a.resident = 0;
+    a.tile = (int)std::min<int64_t>(maxL, limit / (RS * (int64_t)sizeof(float)));
+    smem = a.tile * RS * (int)sizeof(float);
+  }
+  a.rows = rows;
+  a.x = x;
+  a.mean_out = mean_out;
+  a.sd_out = sd_out;
+  a.out_stride = stride;
+  a.sqrt_out = sqrt_out;
+  const bool var = sd_out != nullptr;
+  const bool small = rows < (int64_t)2 * 148 * kLwprBlock * kLwprRows;
+  if (ctx->params_full) {
+    if (var) return small ? launch_lwpr_t<true, true, 2>(ctx, a, smem, st) : launch_lwpr_t<true, true, kLwprRows>(ctx, a, smem, st);
+    return small ? launch_lwpr_t<true, false, 2>(ctx, a, smem, st) : launch_lwpr_t<true, false, kLwprRows>(ctx, a, smem, st);
+  }
+  if (var) return small ? launch_lwpr_t<false, true, 2>(ctx, a, smem, st) : launch_lwpr_t<false, true, kLwprRows>(ctx, a, smem, st);
+  return small ? launch_lwpr_t<false, false, 2>(ctx, a, smem, st) : launch_lwpr_t<false, false, kLwprRows>(ctx, a, smem, st);
+}
+
+bool spread(const pi2_ctx *ctx) {
+  const bool prob = ctx->model == PI2_MODEL_HYBRID_LWPR || ctx->model == PI2_MODEL_TWO_POINT;
+  return prob && ctx->M > 1;
+}
+
+template <int MM>
+int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
+  auto *fn = rollout_kernel<MM>;
+  const int smem = a.N * kRolloutBlock * (int)sizeof(float);
+  TRY(set_smem(ctx, fn, smem));
+  const int64_t grid = (a.K + kRolloutBlock - 1) / kRolloutBlock;
+  fn<<<(unsigned)grid, kRolloutBlock, smem, st>>>(a);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
+int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
+  const int S = a.spread ? a.M : 1;
+  switch (S) {
+    case 1: return launch_rollout_t<1>(ctx, a, st);
+    case 2: return launch_rollout_t<2>(ctx, a, st);
+    case 3: return launch_rollout_t<3>(ctx, a, st);
+    case 4: return launch_rollout_t<4>(ctx, a, st);
+    case 5: return launch_rollout_t<5>(ctx, a, st);
+    case 6: return launch_rollout_t<6>(ctx, a, st);
+    case 7: return launch_rollout_t<7>(ctx, a, st);
+    case 8: return launch_rollout_t<8>(ctx, a, st);
+    default: return launch_rollout_t<0>(ctx, a, st);
+  }
+}
+
+int check_ready(pi2_ctx *ctx) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  if (!ctx->have_dyn) return fail(ctx, PI2_ERR_STATE, "dynamics not set (pi2_set_dynamics)");
+  if (!ctx->have_cost) return fail(ctx, PI2_ERR_STATE, "cost plugin not set (pi2_set_cost)");
+  if (ctx->model == PI2_MODEL_NONE) return fail(ctx, PI2_ERR_STATE, "model plugin not selected");
+  return PI2_OK;
+}
+
+// Fill the pinned StepArgs and queue its H2D copy (waits for the previous one).
+int stage_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, double ceiling,
+               cudaStream_t st) {
+  CU(cudaEventSynchronize(ctx->staged));
+  StepArgs &h = *ctx->h_args;
+  if (state) std::memcpy(h.state, state, sizeof h.state);
+  h.cost = ctx->cost;
+  h.ceiling = ceiling;
+  if (opt) {
+    h.neg_inv_temp = -1.0 / opt->temperature;
+    h.ceiling = opt->cost_ceiling;
+    for (int c = 0; c < 4; ++c) h.std[c] = opt->exploration_std[c];
+    for (int it = 0; it < std::max(1, opt->iterations) && it < PI2_MAX_ITERATIONS; ++it) {
+      derive_key(opt->seed, PI2_STREAM_CONTROL, opt->cycle, (uint64_t)it, h.keys[it][0]);
+      derive_key(opt->seed, PI2_STREAM_DYNAMICS, opt->cycle, (uint64_t)it, h.keys[it][1]);
+    }
+  }
+  CU(cudaMemcpyAsync(ctx->d_args, ctx->h_args, sizeof(StepArgs), cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(ctx->staged, st));
+  return PI2_OK;
+}
+
+int stage_plan(pi2_ctx *ctx, const double *plan, cudaStream_t st) {
+  CU(cudaEventSynchronize(ctx->staged));
+  std::memcpy(ctx->h_plan, plan, sizeof(double) * 4 * ctx->N);
+  CU(cudaMemcpyAsync(ctx->d_plan, ctx->h_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(ctx->staged, st));
+  return PI2_OK;
+}
+
+// rollouts of one iteration: attitude -> LWPR -> rollout/cost
+int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const float *dyn_dev,
+                    double *costs, uint8_t *crash, cudaStream_t st, cudaEvent_t *ev = nullptr) {
+  const int64_t K = ctx->K;
+  const int N = ctx->N;
+  const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
+  const int psmem = 4 * N * (int)sizeof(double);
+  if (noise_dev) {
+    TRY(set_smem(ctx, attitude_kernel<false>, psmem));
+    attitude_kernel<false><<<grid, kRolloutBlock, psmem, st>>>(
+        ctx->d_args, ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp,
+        ctx->d_xin, ctx->d_ang_last, nullptr);
+  } else {
+    TRY(set_smem(ctx, attitude_kernel<true>, psmem));
+    attitude_kernel<true><<<grid, kRolloutBlock, psmem, st>>>(
+        ctx->d_args, ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp,
+        ctx->d_xin, ctx->d_ang_last, nullptr);
+  }
+  CU(cudaGetLastError());
+  if (ev) CU(cudaEventRecord(ev[1], st));
+  const bool sp = spread(ctx);
+  float4 *lw_mean = ctx->d_lw, *lw_std = ctx->d_lw + K * N;
+  if (ctx->model == PI2_MODEL_HYBRID_LWPR)
+    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, reinterpret_cast<float *>(lw_mean),
+                    sp ? reinterpret_cast<float *>(lw_std) : nullptr, 4, 1, st));
+  if (ev) CU(cudaEventRecord(ev[2], st));
+  RollArgs a{};
+  a.sa = ctx->d_args;
+  a.iteration = iteration;
+  a.K = K;
+  a.k_off = ctx->dims.rollout_offset;
+  a.N = N;
+  a.M = ctx->M;
+  a.model = ctx->model;
+  a.spread = sp;
+  a.device_dyn = (sp && dyn_dev == nullptr) ? 1 : 0;
+  a.two_point = (float)ctx->model_param;
+  a.dp = ctx->dp;
+  a.xin = ctx->d_xin;
+  a.ang_last = ctx->d_ang_last;
+  a.lw_mean = lw_mean;
+  a.lw_std = lw_std;
+  a.dyn = dyn_dev;
+  a.costs = costs;
+  a.crash = crash;
+  return launch_rollout(ctx, a, st);
+}
+
+int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
+                   double *plan, cudaStream_t st) {
+  if ((n + kSeg - 1) / kSeg > kSeg) return fail(ctx, PI2_ERR_INVALID, "too many partials (%lld)", (long long)n);
+  const int smem = 2 * kSeg * PI2_PARTIAL_WIDTH * (int)sizeof(double);
+  TRY(set_smem(ctx, combine_kernel, smem));
+  combine_kernel<<<N, 256, smem, st>>>(leaves, n, N, neg_inv, root, plan, ctx->dp);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
+// one full device-noise iteration on the device plan (optionally local-only)
+int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
+                     cudaStream_t st) {
+  TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
+  partials_kernel<<<(unsigned)ctx->n_chunks, 32 * kChunkWarps, 0, st>>>(
+      ctx->d_costs, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+      ctx->d_partials);
+  CU(cudaGetLastError());
+  return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
+                        update_plan ? ctx->d_plan : nullptr, st);
+}
+
+int validate_opt(pi2_ctx *ctx, const pi2_optimize_args *args) {
+  if (!args) return fail(ctx, PI2_ERR_INVALID, "null optimize args");
+  if (!(args->temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
+  for (double s : args->exploration_std)
+    if (!(s > 0)) return fail(ctx, PI2_ERR_INVALID, "exploration_std must be positive");
+  if (args->iterations < 0 || args->iterations > PI2_MAX_ITERATIONS)
+    return fail(ctx, PI2_ERR_INVALID, "iterations must be in [0, %d]", PI2_MAX_ITERATIONS);
+  return PI2_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int pi2_version(void) { return PI2_ABI_VERSION; }
+
+const char *pi2_strerror(int s) {
+  switch (s) {
+    case PI2_OK: return "ok";
+    case PI2_ERR_INVALID: return "invalid argument";
+    case PI2_ERR_STATE: return "invalid state";
+    case PI2_ERR_UNSUPPORTED: return "unsupported plugin";
+    case PI2_ERR_CUDA: return "CUDA error";
+    case PI2_ERR_OOM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+int pi2_device_count(int32_t *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return PI2_OK;
+}
+
+const char *pi2_last_error(const pi2_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_noctx_err.c_str();
+}
+
+int pi2_get_dims(const pi2_ctx *ctx, pi2_dims *out) {
+  if (!ctx || !out) return PI2_ERR_INVALID;
+  *out = ctx->dims;
+  return PI2_OK;
+}
+
+int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
+  pi2_ctx *ctx = nullptr;
+  if (!out || !dims) return fail(nullptr, PI2_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (dims->num_rollouts < 1 || dims->sub_rollouts < 1 || dims->horizon_steps < 1)
+    return fail(nullptr, PI2_ERR_INVALID, "num_rollouts, sub_rollouts, horizon_steps must be >= 1");
+  if (dims->sub_rollouts > PI2_MAX_SUB_ROLLOUTS)
+    return fail(nullptr, PI2_ERR_INVALID, "sub_rollouts must be <= %d", PI2_MAX_SUB_ROLLOUTS);
+  if (dims->horizon_steps > 400) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= 400");
+  if (dims->rollout_offset < 0) return fail(nullptr, PI2_ERR_INVALID, "rollout_offset must be >= 0");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(nullptr, PI2_ERR_CUDA, "no CUDA device available");
+  }
+  if (device < 0 || device >= n) return fail(nullptr, PI2_ERR_INVALID, "device %d out of range", device);
+  ctx = new pi2_ctx();
+  ctx->device = device;
+  ctx->dims = *dims;
+  if (ctx->dims.num_rollouts_total <= 0) ctx->dims.num_rollouts_total = dims->num_rollouts;
+  ctx->K = dims->num_rollouts;
+  ctx->N = dims->horizon_steps;
+  ctx->M = dims->sub_rollouts;
+  int rc = PI2_OK;
+  auto cleanup = [&](int code) {
+    pi2_destroy(ctx);
+    return code;
+  };
+  if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
+  cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  const int64_t K = ctx->K, N = ctx->N;
+  ctx->n_chunks = (K + kChunk - 1) / kChunk;
+#define ALLOC(p, bytes)                                                               \
+  if (cudaMalloc((void **)&(p), (bytes)) != cudaSuccess) {                           \
+    cudaGetLastError();                                                               \
+    g_noctx_err = "device allocation failed: " #p;                                    \
+    return cleanup(PI2_ERR_OOM);                                                      \
+  }
+  ALLOC(ctx->d_args, sizeof(StepArgs));
+  ALLOC(ctx->d_plan, sizeof(double) * 4 * N);
+  ALLOC(ctx->d_plan2, sizeof(double) * 4 * N);
+  ALLOC(ctx->d_xin, sizeof(float4) * K * N);
+  ALLOC(ctx->d_ang_last, sizeof(float4) * K);
+  ALLOC(ctx->d_lw, sizeof(float4) * K * N * 2);
+  ALLOC(ctx->d_costs, sizeof(double) * K * N);
+  ALLOC(ctx->d_crash, K);
+  ALLOC(ctx->d_partials, sizeof(double) * PI2_PARTIAL_WIDTH * ctx->n_chunks * N);
+  ALLOC(ctx->d_root, sizeof(double) * PI2_PARTIAL_WIDTH * N);
+#undef ALLOC
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMallocHost((void **)&ctx->h_args, sizeof(StepArgs)) != cudaSuccess ||
+      cudaMallocHost((void **)&ctx->h_plan, sizeof(double) * 4 * N) != cudaSuccess) {
+    cudaGetLastError();
+    g_noctx_err = "stream/event/pinned allocation failed";
+    return cleanup(PI2_ERR_CUDA);
+  }
+  std::memset(ctx->h_args, 0, sizeof(StepArgs));
+  ctx->h_args->neg_inv_temp = -1.0;
+  ctx->h_args->ceiling = 1e8;
+  cudaEventRecord(ctx->staged, ctx->stream);
+  *out = ctx;
+  return PI2_OK;
+}
+
+void pi2_destroy(pi2_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  invalidate_graph(ctx);
+  void *bufs[] = {ctx->d_params, ctx->d_args,   ctx->d_plan,  ctx->d_plan2,    ctx->d_xin,
+                  ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
+                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch};
+  for (void *p : bufs)
+    if (p) cudaFree(p);
+  if (ctx->h_args) cudaFreeHost(ctx->h_args);
+  if (ctx->h_plan) cudaFreeHost(ctx->h_plan);
+  if (ctx->staged) cudaEventDestroy(ctx->staged);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  cudaGetLastError();
+  delete ctx;
+}
+
+int pi2_set_dynamics(pi2_ctx *ctx, const pi2_dynamics *d) {
+  if (!ctx || !d) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  if (!(d->mass > 0) || !(d->dt > 0) || !(d->rate_gain > 0))
+    return fail(ctx, PI2_ERR_INVALID, "mass, dt and rate_gain must be positive");
+  ctx->dyn = *d;
+  DynParams &p = ctx->dp;
+  p.dt = d->dt;
+  p.gain_dt = d->rate_gain * d->dt;
+  for (int c = 0; c < 4; ++c) {
+    p.lo[c] = d->lo[c];
+    p.hi[c] = d->hi[c];
+  }
+  p.dt32 = (float)d->dt;
+  p.dt2_32 = p.dt32 * p.dt32;
+  p.inv_m32 = (float)(1.0 / d->mass);
+  p.g32 = (float)d->gravity;
+  ctx->have_dyn = true;
+  invalidate_graph(ctx);
+  return PI2_OK;
+}
+
+int pi2_set_lwpr_axis(pi2_ctx *ctx, int32_t axis, int32_t L, int32_t d, const double *centers,
+                      const double *metrics, const double *coefs, const double *lvar) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  if (axis < 0 || axis > 2) return fail(ctx, PI2_ERR_INVALID, "axis must be 0, 1 or 2");
+  if (L < 1) return fail(ctx, PI2_ERR_INVALID, "no receptive fields");
+  if (d < 1 || d > 4) return fail(ctx, PI2_ERR_UNSUPPORTED, "input_dim must be 1..4");
+  if (!centers || !metrics || !coefs || !lvar) return fail(ctx, PI2_ERR_INVALID, "null field array");
+  AxisRaw &a = ctx->axes[axis];
+  a.L = L;
+  a.d = d;
+  a.centers.assign(centers, centers + (size_t)L * d);
+  a.metrics.assign(metrics, metrics + (size_t)L * d * d);
+  a.coefs.assign(coefs, coefs + (size_t)L * (d + 1));
+  a.lvar.assign(lvar, lvar + L);
+  for (double v : a.centers) if (!std::isfinite(v)) return fail(ctx, PI2_ERR_INVALID, "non-finite center");
+  for (double v : a.metrics) if (!std::isfinite(v)) return fail(ctx, PI2_ERR_INVALID, "non-finite metric");
+  for (double v : a.coefs) if (!std::isfinite(v)) return fail(ctx, PI2_ERR_INVALID, "non-finite coefficient");
+  ctx->params_dirty = true;
+  invalidate_graph(ctx);
+  return PI2_OK;
+}
+
+int pi2_select_model(pi2_ctx *ctx, int32_t kind, double param) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  switch (kind) {
+    case PI2_MODEL_HYBRID_LWPR: {
+      const char *names = "xyz";
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ctx->axes[ax].L == 0)
+          return fail(ctx, PI2_ERR_INVALID, "acceleration model for %c axis is untrained", names[ax]);
+        if (ctx->axes[ax].d != 4) return fail(ctx, PI2_ERR_INVALID, "acceleration models take 4 inputs");
+      }
+      break;
+    }
+    case PI2_MODEL_ANALYTIC:
+    case PI2_MODEL_TWO_POINT:
+      break;
+    default:
+      return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown model kind %d", kind);
+  }
+  ctx->model = kind;
+  ctx->model_param = param;
+  invalidate_graph(ctx);
+  return PI2_OK;
+}
+
+int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *c) {
+  if (!ctx || !c) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  if (c->kind != PI2_COST_NAVIGATION && c->kind != PI2_COST_THRESHOLD)
+    return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown cost kind %d", c->kind);
+  if (c->n_obstacles < 0 || c->n_obstacles > PI2_MAX_OBSTACLES)
+    return fail(ctx, PI2_ERR_UNSUPPORTED, "at most %d obstacles", PI2_MAX_OBSTACLES);
+  ctx->cost = *c;
+  ctx->have_cost = true;
+  return PI2_OK;
+}
+
+int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan, const double *noise_dev,
+                        const float *dyn_dev, double ceiling, double *costs_dev, uint8_t *crash_dev,
+                        void *stream) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  if (!state || !plan || !noise_dev || !costs_dev || !crash_dev)
+    return fail(ctx, PI2_ERR_INVALID, "null argument");
+  if (spread(ctx) && !dyn_dev)
+    return fail(ctx, PI2_ERR_INVALID, "probabilistic model with sub_rollouts > 1 needs dyn_noise");
+  cudaStream_t st = pick(ctx, stream);
+  TRY(stage_args(ctx, state, nullptr, ceiling, st));
+  TRY(stage_plan(ctx, plan, st));
+  return launch_rollouts(ctx, 0, noise_dev, dyn_dev, costs_dev, crash_dev, st);
+}
+
+int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise,
+                 const float *dyn, double ceiling, double *costs_out, uint8_t *crash_out) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  if (!state || !plan || !noise || !costs_out || !crash_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  const bool sp = spread(ctx);
+  if (sp && !dyn)
+    return fail(ctx, PI2_ERR_INVALID, "probabilistic model with sub_rollouts > 1 needs dyn_noise");
+  const int64_t K = ctx->K, N = ctx->N, M = ctx->M;
+  cudaStream_t st = ctx->stream;
+  TRY(ensure(ctx, (void **)&ctx->d_noise, &ctx->noise_cap, sizeof(double) * K * N * 4));
+  CU(cudaMemcpyAsync(ctx->d_noise, noise, sizeof(double) * K * N * 4, cudaMemcpyHostToDevice, st));
+  const float *dyn_dev = nullptr;
+  if (sp) {
+    TRY(ensure(ctx, (void **)&ctx->d_dynbuf, &ctx->dyn_cap, sizeof(float) * K * M * N * 3));
+    CU(cudaMemcpyAsync(ctx->d_dynbuf, dyn, sizeof(float) * K * M * N * 3, cudaMemcpyHostToDevice, st));
+    dyn_dev = ctx->d_dynbuf;
+  }
+  TRY(pi2_evaluate_device(ctx, state, plan, ctx->d_noise, dyn_dev, ceiling, ctx->d_costs, ctx->d_crash, st));
+  CU(cudaMemcpyAsync(costs_out, ctx->d_costs, sizeof(double) * K * N, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(crash_out, ctx->d_crash, K, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PI2_OK;
+}
+
+int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const double *costs_dev,
+                      const double *noise_dev, double temperature, double *plan_out, void *stream) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  TRY(bind(ctx));
+  if (!ctx->have_dyn) return fail(ctx, PI2_ERR_STATE, "dynamics not set (pi2_set_dynamics)");
+  if (K < 1 || N < 1 || !plan || !costs_dev || !noise_dev || !plan_out)
+    return fail(ctx, PI2_ERR_INVALID, "batch does not match plan dimensions");
+  if (!(temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
+  cudaStream_t st = pick(ctx, stream);
+  const int64_t chunks = (K + kChunk - 1) / kChunk;
+  const size_t pbytes = sizeof(double) * PI2_PARTIAL_WIDTH * chunks * N;
+  const size_t plbytes = sizeof(double) * 4 * N;
+  TRY(ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, pbytes + plbytes));
+  double *partials = (double *)ctx->d_scratch;
+  double *dplan = partials + PI2_PARTIAL_WIDTH * chunks * N;
+  CU(cudaMemcpyAsync(dplan, plan, plbytes, cudaMemcpyHostToDevice, st));
+  const double neg_inv = -1.0 / temperature;
+  partials_kernel<<<(unsigned)chunks, 32 * kChunkWarps, 0, st>>>(costs_dev, noise_dev, ctx->d_args, 0, K, 0,
+                                                                  N, neg_inv, partials);
+  CU(cudaGetLastError());
+  TRY(launch_combine(ctx, partials, chunks, N, neg_inv, nullptr, dplan, st));
+  CU(cudaMemcpyAsync(plan_out, dplan, plbytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PI2_OK;
+}
+
+int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const double *costs,
+               const double *noise, double temperature, double *plan_out) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  TRY(bind(ctx));
+  if (K < 1 || N < 1 || !costs || !noise) return fail(ctx, PI2_ERR_INVALID, "batch does not match plan dimensions");
+  cudaStream_t st = ctx->stream;
+  TRY(ensure(ctx, (void **)&ctx->d_noise, &ctx->noise_cap, sizeof(double) * K * N * 5));
+  double *dnoise = ctx->d_noise, *dcosts = ctx->d_noise + K * N * 4;
+  CU(cudaMemcpyAsync(dnoise, noise, sizeof(double) * K * N * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(dcosts, costs, sizeof(double) * K * N, cudaMemcpyHostToDevice, st));
+  return pi2_update_device(ctx, K, N, plan, dcosts, dnoise, temperature, plan_out, st);
+}
+
+int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi2_optimize_args *args) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (!state || !plan_inout) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  if (args->iterations == 0) return PI2_OK;  // plan unchanged (test_controller.py:261-265)
+  cudaStream_t st = ctx->stream;
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, state, args, args->cost_ceiling, st));
+  const double neg_inv = -1.0 / args->temperature;
+  std::memcpy(ctx->h_plan, plan_inout, sizeof(double) * 4 * ctx->N);
+  // temperature is baked into the graph's kernel arguments
+  if (args->use_graph && ctx->graph && ctx->graph_iters == args->iterations &&
+      ctx->graph_neg_inv == neg_inv) {
+    CU(cudaGraphLaunch(ctx->graph, st));
+  } else {
+    invalidate_graph(ctx);
+    auto body = [&]() -> int {
+      CU(cudaMemcpyAsync(ctx->d_plan, ctx->h_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyHostToDevice, st));
+      for (int it = 0; it < args->iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
+      CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost, st));
+      return PI2_OK;
+    };
+    if (args->use_graph) {
+      // kernel attributes must be set before capture
+      cudaGraph_t g = nullptr;
+      CU(cudaStreamSynchronize(st));
+      CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const int rc = body();
+      const cudaError_t ec = cudaStreamEndCapture(st, &g);
+      if (rc != PI2_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ec != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
+      const cudaError_t ei = cudaGraphInstantiate(&ctx->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+      ctx->graph_iters = args->iterations;
+      ctx->graph_neg_inv = neg_inv;
+      CU(cudaGraphLaunch(ctx->graph, st));
+    } else {
+      TRY(body());
+    }
+  }
+  CU(cudaStreamSynchronize(st));
+  std::memcpy(plan_inout, ctx->h_plan, sizeof(double) * 4 * ctx->N);
+  return PI2_OK;
+}
+
+int pi2_receding_horizon_step(pi2_ctx *ctx, const double *state, double *plan_inout,
+                              const pi2_optimize_args *args, double *control_out) {
+  TRY(pi2_optimize(ctx, state, plan_inout, args));
+  const int N = ctx->N;
+  if (control_out) std::memcpy(control_out, plan_inout, 4 * sizeof(double));
+  std::memmove(plan_inout, plan_inout + 4, sizeof(double) * 4 * (N - 1));
+  if (N > 1) std::memcpy(plan_inout + 4 * (N - 1), plan_inout + 4 * (N - 2), 4 * sizeof(double));
+  return PI2_OK;
+}
+
+int pi2_load_plan(pi2_ctx *ctx, const double *state, const double *plan, void *stream) {
+  if (!ctx || !plan) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(bind(ctx));
+  cudaStream_t st = pick(ctx, stream);
+  CU(cudaEventSynchronize(ctx->staged));
+  if (state) std::memcpy(ctx->h_args->state, state, sizeof(double) * 12);
+  return stage_plan(ctx, plan, st);
+}
+
+int pi2_read_plan(pi2_ctx *ctx, double *plan_out, void *stream) {
+  if (!ctx || !plan_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(bind(ctx));
+  cudaStream_t st = pick(ctx, stream);
+  CU(cudaMemcpyAsync(plan_out, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PI2_OK;
+}
+
+int pi2_iterate_local(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t iteration, double *root_dev,
+                      void *stream) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (iteration < 0 || iteration >= std::max(1, args->iterations) || !root_dev)
+    return fail(ctx, PI2_ERR_INVALID, "bad iteration index or null partial buffer");
+  cudaStream_t st = pick(ctx, stream);
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, nullptr, args, args->cost_ceiling, st));
+  return launch_iteration(ctx, iteration, -1.0 / args->temperature, root_dev, false, st);
+}
+
+int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (reps < 1 || !stage_ms) return fail(ctx, PI2_ERR_INVALID, "reps must be >= 1");
+  cudaStream_t st = ctx->stream;
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, nullptr, args, args->cost_ceiling, st));
+  cudaEvent_t ev[6];
+  for (auto &e : ev) CU(cudaEventCreate(&e));
+  const double neg_inv = -1.0 / args->temperature;
+  double acc[5] = {0, 0, 0, 0, 0};
+  int rc = PI2_OK;
+  for (int r = 0; r < reps && rc == PI2_OK; ++r) {
+    cudaEventRecord(ev[0], st);
+    rc = launch_rollouts(ctx, 0, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, ev);
+    if (rc != PI2_OK) break;
+    cudaEventRecord(ev[3], st);
+    partials_kernel<<<(unsigned)ctx->n_chunks, 32 * kChunkWarps, 0, st>>>(
+        ctx->d_costs, nullptr, ctx->d_args, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+        ctx->d_partials);
+    cudaEventRecord(ev[4], st);
+    rc = launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, ctx->d_root, nullptr, st);
+    cudaEventRecord(ev[5], st);
+    if (cudaEventSynchronize(ev[5]) != cudaSuccess) rc = fail(ctx, PI2_ERR_CUDA, "profile: %s", cudaGetErrorString(cudaGetLastError()));
+    for (int i = 0; i < 5 && rc == PI2_OK; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      acc[i] += ms;
+    }
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  TRY(rc);
+  for (int i = 0; i < 5; ++i) stage_ms[i] = acc[i] / reps;
+  return PI2_OK;
+}
+
+int pi2_iterate_finalize(pi2_ctx *ctx, const double *gathered, int32_t world, double temperature,
+                         void *stream) {
+  if (!ctx || !gathered || world < 1) return fail(ctx, PI2_ERR_INVALID, "bad gathered partials");
+  TRY(bind(ctx));
+  if (!(temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
+  return launch_combine(ctx, gathered, world, ctx->N, -1.0 / temperature, nullptr, ctx->d_plan,
+                        pick(ctx, stream));
+}
+
+int64_t pi2_partial_chunk(void) { return kChunk; }
+
+int pi2_chunk_partials_host(const double *costs, const double *noise, int64_t K, int32_t N,
+                            double temperature, double *out) {
+  if (!costs || !noise || !out || K < 1 || N < 1 || !(temperature > 0)) return PI2_ERR_INVALID;
+  const double neg_inv = -1.0 / temperature;
+  const int64_t chunks = (K + kChunk - 1) / kChunk;
+  for (int64_t c = 0; c < chunks; ++c)
+    for (int t = 0; t < N; ++t) {
+      double m = INFINITY;
+      const int64_t k0 = c * kChunk, k1 = std::min<int64_t>(K, k0 + kChunk);
+      for (int64_t k = k0; k < k1; ++k) m = std::min(m, costs[k * N + t]);
+      double z = 0, v[4] = {0, 0, 0, 0};
+      for (int64_t k = k0; k < k1; ++k) {
+        const double w = std::exp((costs[k * N + t] - m) * neg_inv);
+        z += w;
+        for (int q = 0; q < 4; ++q) v[q] += w * noise[(k * N + t) * 4 + q];
+      }
+      double *o = out + (c * N + t) * PI2_PARTIAL_WIDTH;
+      o[0] = m; o[1] = z;
+      for (int q = 0; q < 4; ++q) o[2 + q] = v[q];
+    }
+  return PI2_OK;
+}
+
+int pi2_combine_partials_host(const double *partials, int64_t count, int32_t N, double temperature,
+                              double *out) {
+  if (!partials || !out || count < 1 || N < 1 || !(temperature > 0)) return PI2_ERR_INVALID;
+  const double neg_inv = -1.0 / temperature;
+  std::vector<double> v((size_t)count * PI2_PARTIAL_WIDTH);
+  for (int t = 0; t < N; ++t) {
+    for (int64_t i = 0; i < count; ++i)
+      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c)
+        v[(size_t)i * PI2_PARTIAL_WIDTH + c] = partials[(i * N + t) * PI2_PARTIAL_WIDTH + c];
+    // the device tree: segments of kSeg leaves, then the segment roots
+    const int64_t nseg = (count + kSeg - 1) / kSeg;
+    std::vector<double> roots((size_t)nseg * PI2_PARTIAL_WIDTH);
+    auto tree = [&](double *base, int64_t n) {
+      for (int64_t st = 1; st < n; st <<= 1)
+        for (int64_t i = 0; i + st < n; i += 2 * st)
+          partial_combine(base + i * PI2_PARTIAL_WIDTH, base + (i + st) * PI2_PARTIAL_WIDTH, neg_inv);
+    };
+    for (int64_t s = 0; s < nseg; ++s) {
+      const int64_t cnt = std::min<int64_t>(kSeg, count - s * kSeg);
+      tree(v.data() + s * kSeg * PI2_PARTIAL_WIDTH, cnt);
+      std::memcpy(&roots[(size_t)s * PI2_PARTIAL_WIDTH], v.data() + s * kSeg * PI2_PARTIAL_WIDTH,
+                  sizeof(double) * PI2_PARTIAL_WIDTH);
+    }
+    tree(roots.data(), nseg);
+    std::memcpy(out + (size_t)t * PI2_PARTIAL_WIDTH, roots.data(), sizeof(double) * PI2_PARTIAL_WIDTH);
+  }
+  return PI2_OK;
+}
+
+int pi2_device_noise(pi2_ctx *ctx, int32_t which, uint64_t seed, uint64_t cycle, uint64_t iteration,
+                     const double *std_, void *out_host) {
+  if (!ctx || !out_host) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  if (which != PI2_STREAM_CONTROL && which != PI2_STREAM_DYNAMICS)
+    return fail(ctx, PI2_ERR_INVALID, "unknown noise stream %d", which);
+  TRY(bind(ctx));
+  cudaStream_t st = ctx->stream;
+  pi2_optimize_args a{};
+  a.temperature = 1.0;
+  a.cost_ceiling = 1e8;
+  for (int c = 0; c < 4; ++c) a.exploration_std[c] = std_ ? std_[c] : 1.0;
+  a.seed = seed;
+  a.cycle = cycle;
+  a.iterations = 1;
+  CU(cudaEventSynchronize(ctx->staged));
+  StepArgs &h = *ctx->h_args;
+  for (int c = 0; c < 4; ++c) h.std[c] = a.exploration_std[c];
+  derive_key(seed, PI2_STREAM_CONTROL, cycle, iteration, h.keys[0][0]);
+  derive_key(seed, PI2_STREAM_DYNAMICS, cycle, iteration, h.keys[0][1]);
+  CU(cudaMemcpyAsync(ctx->d_args, ctx->h_args, sizeof(StepArgs), cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(ctx->staged, st));
+  const int64_t K = ctx->K, N = ctx->N, M = ctx->M;
+  const int64_t n = which == PI2_STREAM_CONTROL ? K * N : K * M * N;
+  const size_t bytes = which == PI2_STREAM_CONTROL ? sizeof(double) * n * 4 : sizeof(float) * n * 3;
+  TRY(ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, bytes));
+  noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      ctx->d_args, which, 0, K, ctx->dims.rollout_offset, (int)N, (int)M, (double *)ctx->d_scratch,
+      (float *)ctx->d_scratch);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(out_host, ctx->d_scratch, bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PI2_OK;
+}
+
+int pi2_lwpr_predict(pi2_ctx *ctx, int32_t axis, int64_t rows, const float *X, float *mean_out,
+                     float *var_out) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  if (axis < 0 || axis > 2 || ctx->axes[axis].L == 0) return fail(ctx, PI2_ERR_INVALID, "no receptive fields");
+  if (rows < 1 || !X || !mean_out) return fail(ctx, PI2_ERR_INVALID, "X must have shape (B, input_dim)");
+  TRY(bind(ctx));
+  const int d = ctx->axes[axis].d;
+  cudaStream_t st = ctx->stream;
+  std::vector<float4> xp((size_t)rows);
+  for (int64_t r = 0; r < rows; ++r) {
+    float v[4] = {0, 0, 0, 0};
+    for (int i = 0; i < d; ++i) v[i] = X[r * d + i];
+    xp[r] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  const size_t xb = sizeof(float4) * rows, ob = sizeof(float) * rows;
+  TRY(ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, xb + 2 * ob));
+  float4 *dx = (float4 *)ctx->d_scratch;
+  float *dm = (float *)(dx + rows), *dv = dm + rows;
+  CU(cudaMemcpyAsync(dx, xp.data(), xb, cudaMemcpyHostToDevice, st));
+  TRY(launch_lwpr(ctx, axis, axis + 1, rows, dx, dm, var_out ? dv : nullptr, 1, 0, st));
+  CU(cudaMemcpyAsync(mean_out, dm, ob, cudaMemcpyDeviceToHost, st));
+  if (var_out) CU(cudaMemcpyAsync(var_out, dv, ob, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PI2_OK;
+}
+
+}  // extern "C"

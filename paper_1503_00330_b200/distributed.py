@@ -1,0 +1,113 @@
+"""Rollout sharding across GPUs (one process per GPU, torch.distributed).
+
+The reference parallelises rollouts over a thread pool in fixed chunks so
+results never depend on the worker count (controller.py:10-13, 214-242).
+Here rank r of G owns a contiguous, chunk-aligned slice of the K rollouts;
+every iteration it produces one (min S, Z, V[4]) partial per timestep for
+its slice (``pi2_iterate_local``), the G partials are all-gathered (NCCL
+over NVLink, ~6·N·8 bytes per rank) and every rank applies the same
+fixed-order tree combine and plan update (``pi2_iterate_finalize``).  With
+power-of-two chunk counts per rank the tree is exactly the single-GPU tree,
+so the update is bitwise identical for 1/2/4/8 GPUs.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _abi
+from .controller import ControlPlan, PiConfig, dynamics_struct, model_kind, optimize_args
+from .lwpr import stage_axis
+from .simworld import cost_struct
+
+
+def shard_range(num_rollouts: int, rank: int, world: int, chunk: int | None = None) -> tuple[int, int]:
+    """[start, stop) of rank's rollouts: contiguous, chunk-aligned, sizes differ by <= one chunk."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    chunk = int(chunk or _abi.lib().pi2_partial_chunk())
+    n_chunks = -(-num_rollouts // chunk)
+    base, extra = divmod(n_chunks, world)
+    c0 = rank * base + min(rank, extra)
+    c1 = c0 + base + (1 if rank < extra else 0)
+    return min(c0 * chunk, num_rollouts), min(c1 * chunk, num_rollouts)
+
+
+def gather_partials(partial, group=None):
+    """All-gather a (N, 6) partial from every rank into (G, N, 6), rank order."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
+    dist.all_gather_into_tensor(out, partial.contiguous(), group=group)
+    return out
+
+
+def combine_gathered_host(gathered: np.ndarray, temperature: float) -> np.ndarray:
+    """Fixed-order combine of (G, N, 6) partials on the host (same tree as the device)."""
+    g = np.ascontiguousarray(gathered, dtype=np.float64)
+    out = np.empty(g.shape[1:])
+    _abi.check(_abi.lib().pi2_combine_partials_host(_abi.ptr(g), g.shape[0], g.shape[1],
+                                                    float(temperature), _abi.ptr(out)))
+    return out
+
+
+def apply_partial(plan: np.ndarray, root: np.ndarray, lo, hi) -> np.ndarray:
+    """plan + V/Z clipped to the bounds (controller.py:369-371) — host form of the finalize."""
+    return np.clip(plan + root[:, 2:6] / root[:, 1:2], lo[None, :], hi[None, :])
+
+
+class ShardedEngine:
+    """This rank's share of a PI²-RH optimisation with device noise.
+
+    ``optimize(state, plan, cost_model, cycle_index)`` has the semantics of
+    ``controller.optimize`` with a ``noise="device"`` engine; all ranks return
+    the same plan.
+    """
+
+    def __init__(self, model, config: PiConfig, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.config = config
+        self.model = model
+        self.params = model.params
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.start, self.stop = shard_range(config.num_rollouts, self.rank, self.world)
+        if self.stop <= self.start:
+            raise ValueError("more ranks than rollout chunks")
+        kind, param = model_kind(model)
+        self.ctx = _abi.Context(self.device, self.stop - self.start, config.horizon_steps,
+                                config.sub_rollouts, rollout_offset=self.start,
+                                num_rollouts_total=config.num_rollouts)
+        if kind == _abi.MODEL_HYBRID_LWPR:
+            for a in range(3):
+                stage_axis(self.ctx, a, model.models[a])
+        self.ctx.call("pi2_select_model", kind, param)
+        dev = torch.device("cuda", self.device)
+        self.partial = torch.empty((config.horizon_steps, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=dev)
+
+    def optimize(self, state, plan: ControlPlan, cost_model, cycle_index: int = 0) -> ControlPlan:
+        import torch
+
+        cfg = self.config
+        if cfg.iterations_per_step == 0:
+            return plan
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
+        self.ctx.call("pi2_set_cost", cost_struct(cost_model))
+        args = optimize_args(cfg, cycle_index, use_graph=False)
+        controls = np.ascontiguousarray(plan.controls, dtype=np.float64).copy()
+        self.ctx.call("pi2_load_plan", _abi.ptr(np.ascontiguousarray(state.as_array())), _abi.ptr(controls),
+                      _abi.ptr(stream))
+        for it in range(cfg.iterations_per_step):
+            self.ctx.call("pi2_iterate_local", args, it, _abi.ptr(self.partial), _abi.ptr(stream))
+            gathered = gather_partials(self.partial, self.group)
+            self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, float(cfg.temperature),
+                          _abi.ptr(torch.cuda.current_stream(self.device).cuda_stream))
+        self.ctx.call("pi2_read_plan", _abi.ptr(controls), _abi.ptr(stream))
+        return plan.replaced(controls)

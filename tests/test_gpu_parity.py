@@ -1,0 +1,372 @@
+"""Parity of the CUDA path (through the C ABI) with the reference and the oracle.
+
+Gates (BASELINE.json north star): per-rollout costs-to-go within 1e-5
+relative, crash flags exact, control update Δu within 1e-4 per channel
+(normalised by the channel's max |Δu|).  Golden fixtures
+come from the real reference (tests/golden/make_golden.py); larger cases
+compare against the numpy oracle run on this host.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1503_00330_b200 as P
+from paper_1503_00330_b200 import _abi, synthetic
+from oracle import lwpr as OL
+from oracle import rollout as RO
+from tests._cases import TASK_OBSTACLES, TASK_WAYPOINTS, eval_case_names, load, stacks_from
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL = 1e-5
+DU_TOL = 1e-4
+
+
+def cost_rel_err(got, want):
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
+
+
+def du_err(new, want, plan):
+    du, wdu = new - plan, want - plan
+    scale = np.maximum(np.max(np.abs(wdu), axis=0), 1e-300)
+    return np.max(np.abs(du - wdu), axis=0) / scale
+
+
+def model_of(z):
+    if bool(z["analytic"]):
+        return P.AnalyticModel(P.QuadParams())
+    return P.HybridModel.from_stacks(stacks_from(z), P.QuadParams())
+
+
+def gpu_eval(z, model=None, engine_kw=None):
+    M = int(z["M"])
+    model = model or model_of(z)
+    cfg = P.PiConfig(num_rollouts=int(z["K"]), sub_rollouts=M, horizon_steps=int(z["N"]), iterations_per_step=1,
+                     exploration_std=z["std"], rng_seed=int(z["seed"]))
+    eng = P.RolloutEngine(model, cfg, device=0, **(engine_kw or {}))
+    task = P.Task.default()
+    plan = P.ControlPlan(z["plan"], 0.02, 0.0, *P.QuadParams().control_bounds())
+    dyn = z["dyn"] if z["dyn"].size else None
+    b = eng.evaluate(P.QuadState.from_array(z["state"]), plan, z["noise"],
+                     P.RolloutCost(task, int(z["waypoint_index"])), dyn)
+    return b, plan
+
+
+def test_device_present():
+    assert _abi.device_count() >= 1, "GPU tests need a CUDA device"
+
+
+@pytest.mark.parametrize("name", eval_case_names())
+def test_evaluate_matches_reference_golden(name):
+    z = load("eval_" + name)
+    b, plan = gpu_eval(z)
+    want = z["costs"]
+    ceil = want == float(z["ceiling"])
+    np.testing.assert_array_equal(b.costs_to_go == float(z["ceiling"]), ceil)
+    np.testing.assert_array_equal(b.crash_flags, z["crash"])
+    if (~ceil).any():
+        assert cost_rel_err(b.costs_to_go[~ceil], want[~ceil]) < COST_RTOL
+    new = P.path_integral_update(plan, b, float(z["temperature"]))
+    assert np.all(du_err(new.controls, z["new_plan"], z["plan"]) < DU_TOL)
+
+
+@pytest.mark.parametrize("K,N,L,M,full", [(2048, 50, 100, 4, False), (1500, 50, 100, 1, False),
+                                          (777, 20, 40, 3, True), (300, 10, 20, 16, False),
+                                          (1, 1, 5, 1, False), (129, 7, 9, 8, False)])
+def test_evaluate_matches_oracle(K, N, L, M, full):
+    stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=K)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn + np.array([0.05, -0.1, 0.07]))
+    plan = P.ControlPlan.hover(params, N)
+    noise = P.sample_noise(cfg, 1, 0)
+    dyn = P.sample_dynamics_noise(cfg, 1, 0) if M > 1 else None
+    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, noise, P.RolloutCost(task, 2), dyn)
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise,
+                         RO.Cost(TASK_WAYPOINTS[2], TASK_OBSTACLES), dyn, M)
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+    new = P.path_integral_update(plan, b, 1.0)
+    assert np.all(du_err(new.controls, RO.update(plan.controls, lo, hi, rc, noise, 1.0), plan.controls) < DU_TOL)
+
+
+def test_frozen_lwpr_predict_matches_reference():
+    z = load("lwpr")
+    st = stacks_from(z, "diag_")
+    X = z["diag_X"]
+    for a in range(3):
+        fr = P.FrozenLwpr(P.LwprModel.from_stack(st[a].centers, st[a].metrics, st[a].coefs, st[a].lvar), len(X))
+        m = np.empty(len(X), np.float32)
+        v = np.empty(len(X), np.float32)
+        fr.predict_into(X, m, v)
+        np.testing.assert_allclose(m, z[f"diag_mean{a}"], rtol=2e-5, atol=2e-5)
+        np.testing.assert_allclose(v, z[f"diag_var{a}"], rtol=2e-4, atol=2e-6)
+    for i in range(int(z["n_full"])):
+        mdl = P.LwprModel.from_stack(z[f"full{i}_centers"], z[f"full{i}_metrics"], z[f"full{i}_coefs"],
+                                     z[f"full{i}_lvar"])
+        Xf = z[f"full{i}_X"]
+        fr = P.FrozenLwpr(mdl, len(Xf))
+        m = np.empty(len(Xf), np.float32)
+        v = np.empty(len(Xf), np.float32)
+        fr.predict_into(Xf, m, v)
+        scale = max(1.0, float(np.abs(z[f"full{i}_mean"]).max()))
+        np.testing.assert_allclose(m, z[f"full{i}_mean"], atol=2e-5 * scale)
+        np.testing.assert_allclose(v, z[f"full{i}_var"], atol=2e-5 * scale, rtol=1e-4)
+
+
+def test_frozen_lwpr_far_rows_follow_float32_underflow():
+    """Rows whose every weight is a float32 denormal or zero."""
+    z = load("eval_far_m1")
+    st = stacks_from(z)
+    rng = np.random.default_rng(5)
+    X = rng.uniform([-1.5, -1.5, -1.5, 0.0], [1.5, 1.5, 1.5, 0.37], size=(4096, 4)).astype(np.float32)
+    for a in range(3):
+        p = OL.fold(st[a].centers, st[a].metrics, st[a].coefs, st[a].lvar)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            rm, rv = OL.predict_f32(p, X)
+        fr = P.FrozenLwpr(P.LwprModel.from_stack(st[a].centers, st[a].metrics, st[a].coefs, st[a].lvar), len(X))
+        m = np.empty(len(X), np.float32)
+        v = np.empty(len(X), np.float32)
+        fr.predict_into(X, m, v)
+        np.testing.assert_array_equal(np.isnan(m), np.isnan(rm))
+        ok = ~np.isnan(rm)
+        np.testing.assert_allclose(m[ok], rm[ok], rtol=1e-3, atol=1e-3)
+
+
+def test_update_known_answers():
+    z = load("update")
+    plan = P.ControlPlan.hover(P.QuadParams(), 3)
+    new = P.path_integral_update(plan, P.RolloutBatch(z["hand_noise"], z["hand_costs"], np.zeros(2, bool)), 1.0)
+    np.testing.assert_allclose(new.controls, z["hand_new"], atol=1e-12)
+    for i in range(int(z["n_random"])):
+        n = z[f"r{i}_plan"].shape[0]
+        plan = P.ControlPlan.hover(P.QuadParams(), n)
+        b = P.RolloutBatch(z[f"r{i}_noise"], z[f"r{i}_costs"], np.zeros(len(z[f"r{i}_costs"]), bool))
+        new = P.path_integral_update(plan, b, float(z[f"r{i}_lambda"]))
+        np.testing.assert_allclose(new.controls - plan.controls, z[f"r{i}_new"] - plan.controls,
+                                   rtol=1e-9, atol=1e-12)
+
+
+def test_update_shape_errors():
+    plan = P.ControlPlan.hover(P.QuadParams(), 4)
+    with pytest.raises(ValueError, match="batch does not match"):
+        P.path_integral_update(plan, P.RolloutBatch(np.zeros((3, 5, 4)), np.zeros((3, 5)), np.zeros(3, bool)), 1.0)
+
+
+def test_optimize_and_receding_horizon_match_reference():
+    z = load("optimize")
+    model = P.HybridModel.from_stacks(stacks_from(z), P.QuadParams())
+    cfg = P.PiConfig(num_rollouts=int(z["K"]), sub_rollouts=int(z["M"]), horizon_steps=int(z["N"]),
+                     iterations_per_step=int(z["iterations"]), rng_seed=int(z["seed"]), chunk_size=16)
+    task = P.Task.default()
+    state = P.QuadState.from_array(z["state"])
+    plan = P.ControlPlan.hover(P.QuadParams(), int(z["N"]))
+    cost = P.RolloutCost(task, int(z["waypoint_index"]))
+    opt = P.optimize(state, plan, cfg, model, cost, cycle_index=int(z["cycle"]))
+    assert np.all(du_err(opt.controls, z["optimized"], plan.controls) < DU_TOL)
+    ctrl, carried = P.receding_horizon_step(state, plan, cfg, model, cost, cycle_index=int(z["cycle"]))
+    np.testing.assert_allclose(ctrl.as_array(), z["control"], rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(carried.controls, z["carried"], rtol=1e-4, atol=1e-6)
+
+
+def test_zero_variance_subrollouts_equal_mean_exactly():
+    """Reference test_controller.py:143-169 on the GPU engine."""
+    p = P.QuadParams()
+    models = [P.LwprModel.from_stack([[0.0, 0.0, 0.0, p.hover_thrust]], [np.diag(np.ones(4))],
+                                     [[0.3, 0, 0, 0, 0]], [0.0]) for _ in range(3)]
+    hybrid = P.HybridModel(tuple(models), p)
+    task = P.Task(waypoints=np.array([[0.0, 0.0, 1.0]]), obstacles=np.empty((0, 2)), laps=1)
+    plan = P.ControlPlan.hover(p, 12)
+    cfg = P.PiConfig(num_rollouts=8, horizon_steps=12, sub_rollouts=8, rng_seed=7,
+                     exploration_std=[1.5, 1.5, 0.6, 0.04])
+    noise = P.sample_noise(cfg, 0, 0)
+    dyn = P.sample_dynamics_noise(cfg, 0, 0)
+    state = P.QuadState.hover((0, 0, 1))
+    a = P.evaluate_rollouts(state, plan, noise, hybrid, P.RolloutCost(task, 0), sub_rollouts=8, dyn_noise=dyn)
+    b = P.evaluate_rollouts(state, plan, noise, hybrid, P.RolloutCost(task, 0), sub_rollouts=1)
+    np.testing.assert_array_equal(a.costs_to_go, b.costs_to_go)
+
+
+class TwoPointModel:
+    """Reference tests/synthetic.py:17-40 (the engine maps it to the device two-point model)."""
+
+    probabilistic = True
+    noise_transform = staticmethod(np.sign)
+
+    def __init__(self, magnitude, params=None):
+        self.params = params or P.QuadParams()
+        self.magnitude = float(magnitude)
+
+
+class ThresholdCost:
+    def __init__(self, threshold):
+        self.threshold = np.float32(threshold)
+
+
+def two_point_expected_cost(magnitude, threshold, n_steps, dt):
+    total = 0.0
+    for bits in range(1 << n_steps):
+        z = v = s = 0.0
+        for t in range(n_steps):
+            z = z + v * dt
+            v = v + (magnitude if (bits >> t) & 1 else -magnitude) * dt
+            if z > threshold:
+                s += dt
+        total += s
+    return total / (1 << n_steps)
+
+
+def test_two_point_model_matches_enumeration():
+    """Reference test_controller.py:171-189 on the GPU engine."""
+    p = P.QuadParams()
+    n, mag, thr = 10, 2.0, -0.0043
+    cfg = P.PiConfig(num_rollouts=4000, horizon_steps=n, sub_rollouts=4, rng_seed=5)
+    noise = np.zeros((4000, n, 4))
+    dyn = P.sample_dynamics_noise(cfg, 0, 0)
+    b = P.evaluate_rollouts(P.QuadState.hover((0, 0, 0)), P.ControlPlan.hover(p, n), noise, TwoPointModel(mag, p),
+                            ThresholdCost(thr), sub_rollouts=4, dyn_noise=dyn)
+    got = b.costs_to_go[:, 0]
+    assert abs(got.mean() - two_point_expected_cost(mag, thr, n, p.dt)) < 5 * got.std() / np.sqrt(len(got)) + 1e-9
+
+
+def test_subrollout_cost_variance_scales_inverse_m():
+    """Reference test_controller.py:308-327 on the GPU engine (M=64 uses the generic kernel)."""
+    p = P.QuadParams()
+    stds = {}
+    for m_sub in (4, 16, 64):
+        cfg = P.PiConfig(num_rollouts=1500, horizon_steps=10, sub_rollouts=m_sub, rng_seed=3)
+        dyn = P.sample_dynamics_noise(cfg, 0, 0)
+        b = P.evaluate_rollouts(P.QuadState.hover((0, 0, 0)), P.ControlPlan.hover(p, 10), np.zeros((1500, 10, 4)),
+                                TwoPointModel(2.0, p), ThresholdCost(-0.0043), sub_rollouts=m_sub, dyn_noise=dyn)
+        stds[m_sub] = b.costs_to_go[:, 0].std()
+    assert stds[16] == pytest.approx(stds[4] / 2.0, rel=0.25)
+    assert stds[64] == pytest.approx(stds[16] / 2.0, rel=0.25)
+
+
+def test_engine_errors_match_reference():
+    p = P.QuadParams()
+    model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(8), p)
+    cfg = P.PiConfig(num_rollouts=4, horizon_steps=5, sub_rollouts=2)
+    eng = P.RolloutEngine(model, cfg, device=0)
+    plan = P.ControlPlan.hover(p, 5)
+    cost = P.RolloutCost(P.Task.default(), 0)
+    with pytest.raises(ValueError, match="noise horizon"):
+        eng.evaluate(P.QuadState.hover((0, 0, 1)), plan, np.zeros((4, 6, 4)), cost, np.zeros((4, 2, 6, 3), np.float32))
+    with pytest.raises(ValueError, match="needs dyn_noise"):
+        eng.evaluate(P.QuadState.hover((0, 0, 1)), plan, np.zeros((4, 5, 4)), cost)
+    untrained = P.HybridModel(tuple(P.LwprModel(4) for _ in range(3)), p)
+    with pytest.raises(ValueError, match="untrained"):
+        P.RolloutEngine(untrained, cfg, device=0).evaluate(P.QuadState.hover((0, 0, 1)), plan, np.zeros((4, 5, 4)),
+                                                           cost, np.zeros((4, 2, 5, 3), np.float32))
+
+
+# ---------------------------------------------------------------- device noise
+def test_device_noise_statistics_and_addressing():
+    params = P.QuadParams()
+    model = P.AnalyticModel(params)
+    cfg = P.PiConfig(num_rollouts=10_000, horizon_steps=50, sub_rollouts=4)
+    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+    ctx = eng.context(cfg.num_rollouts, cfg.horizon_steps)
+    std = np.array([1.5, 1.5, 0.6, 0.04])
+
+    def draw(cycle, it, seed=7):
+        out = np.empty((cfg.num_rollouts, cfg.horizon_steps, 4))
+        ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, seed, cycle, it, _abi.ptr(std), _abi.ptr(out))
+        return out
+
+    a = draw(3, 1)
+    np.testing.assert_array_equal(a, draw(3, 1))
+    assert not np.array_equal(a, draw(4, 1)) and not np.array_equal(a, draw(3, 0))
+    assert not np.array_equal(a, draw(3, 1, seed=8))
+    np.testing.assert_allclose(a.std(axis=(0, 1)), std, rtol=0.02)
+    np.testing.assert_allclose(a.mean(axis=(0, 1)) / std, 0.0, atol=0.01)
+    d = np.empty((cfg.num_rollouts, 4, cfg.horizon_steps, 3), np.float32)
+    ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, 7, 3, 1, None, _abi.ptr(d))
+    np.testing.assert_allclose(d.std(), 1.0, rtol=0.01)
+    np.testing.assert_allclose(d.mean(), 0.0, atol=0.01)
+    z = d.reshape(-1).astype(np.float64)
+    assert abs(np.mean(z ** 4) - 3.0) < 0.05  # Gaussian kurtosis
+
+
+def _device_setup(K=3000, N=40, L=48, M=4, iters=2):
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=9), params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=iters, rng_seed=11)
+    task = P.Task.default()
+    return params, model, cfg, task, P.QuadState.hover(task.spawn), P.ControlPlan.hover(params, N), P.RolloutCost(task, 1)
+
+
+def test_device_optimize_equals_materialised_noise_path():
+    """Fused device-noise optimize == evaluate + update fed with the same device noise."""
+    params, model, cfg, task, state, plan, cost = _device_setup(iters=1)
+    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+    fused = eng.optimize_device(state, plan, cost, cycle_index=4)
+    ctx = eng.context(cfg.num_rollouts, cfg.horizon_steps)
+    eps = np.empty((cfg.num_rollouts, cfg.horizon_steps, 4))
+    ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, cfg.rng_seed, 4, 0, _abi.ptr(cfg.exploration_std), _abi.ptr(eps))
+    dyn = np.empty((cfg.num_rollouts, cfg.sub_rollouts, cfg.horizon_steps, 3), np.float32)
+    ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, cfg.rng_seed, 4, 0, None, _abi.ptr(dyn))
+    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, eps, cost, dyn)
+    two_step = P.path_integral_update(plan, b, cfg.temperature)
+    np.testing.assert_array_equal(fused.controls, two_step.controls)
+    # and the oracle agrees on those inputs
+    om = RO.Model(synthetic.hybrid_stacks(48, seed=9))
+    lo, hi = om.dyn.bounds()
+    rc, _ = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, eps,
+                        RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES), dyn, cfg.sub_rollouts)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
+def test_graph_replay_matches_eager_and_is_deterministic():
+    params, model, cfg, task, state, plan, cost = _device_setup()
+    g = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=True)
+    e = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=False)
+    outs = [g.optimize_device(state, plan, cost, c) for c in (0, 1, 0)]
+    np.testing.assert_array_equal(outs[0].controls, outs[2].controls)
+    assert not np.array_equal(outs[0].controls, outs[1].controls)
+    np.testing.assert_array_equal(outs[0].controls, e.optimize_device(state, plan, cost, 0).controls)
+
+
+def test_sharded_partials_are_gpu_count_invariant():
+    """Rank shards evaluated one after another on one GPU (no cross-waiting kernels):
+    the fixed-order combine gives the single-context plan bitwise for G = 2 and 4."""
+    from paper_1503_00330_b200.controller import dynamics_struct, optimize_args
+    from paper_1503_00330_b200.distributed import shard_range
+    from paper_1503_00330_b200.lwpr import stage_axis
+    from paper_1503_00330_b200.simworld import cost_struct
+
+    params, model, cfg, task, state, plan, cost = _device_setup(K=4096, iters=1)
+    single = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=False).optimize_device(state, plan, cost, 2)
+    args = optimize_args(cfg, 2, use_graph=False)
+    for world in (2, 4):
+        ctxs, parts = [], []
+        for r in range(world):
+            s, e = shard_range(cfg.num_rollouts, r, world)
+            c = _abi.Context(0, e - s, cfg.horizon_steps, cfg.sub_rollouts, rollout_offset=s,
+                             num_rollouts_total=cfg.num_rollouts)
+            for a in range(3):
+                stage_axis(c, a, model.models[a])
+            c.call("pi2_select_model", _abi.MODEL_HYBRID_LWPR, 0.0)
+            c.call("pi2_set_dynamics", dynamics_struct(params, plan.lo, plan.hi))
+            c.call("pi2_set_cost", cost_struct(cost))
+            c.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan.controls)), None)
+            import torch
+
+            part = torch.empty((cfg.horizon_steps, 6), dtype=torch.float64, device="cuda:0")
+            c.call("pi2_iterate_local", args, 0, _abi.ptr(part), None)
+            torch.cuda.synchronize()
+            ctxs.append(c)
+            parts.append(part)
+        import torch
+
+        gathered = torch.stack(parts).contiguous()
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.call("pi2_iterate_finalize", _abi.ptr(gathered), world, float(cfg.temperature), None)
+            out = np.empty((cfg.horizon_steps, 4))
+            c.call("pi2_read_plan", _abi.ptr(out), None)
+            np.testing.assert_array_equal(out, single.controls)
