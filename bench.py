@@ -228,8 +228,9 @@ def run_ours(args, rank: int, world: int, local: int):
     state = P.QuadState.hover(task.spawn)
     plan0 = P.ControlPlan.hover(params, T)
     cost = P.RolloutCost(task, 1)
-    stream = torch.cuda.current_stream(local)
-    sptr = _abi.ptr(stream.cuda_stream)
+    stream = torch.cuda.Stream(device=local)  # dedicated stream: kernels, events and NCCL share it
+    torch.cuda.set_stream(stream)
+    sptr = _abi.torch_stream(local)
 
     if world > 1:
         from paper_1503_00330_b200.distributed import ShardedEngine, gather_partials

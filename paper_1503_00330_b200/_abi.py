@@ -135,6 +135,22 @@ def ptr(a) -> C.c_void_p | None:
     raise TypeError(f"cannot pass {type(a).__name__} to the C ABI")
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream
+
+
+def torch_stream(device=None) -> C.c_void_p:
+    """ABI stream handle of torch's current stream on ``device``.
+
+    torch reports its default stream as handle 0, which the ABI would read as
+    "the context's own stream"; map it to cudaStreamLegacy so kernels, torch
+    events and torch collectives really share one stream.
+    """
+    import torch
+
+    h = torch.cuda.current_stream(device).cuda_stream
+    return C.c_void_p(h if h else CUDA_STREAM_LEGACY)
+
+
 def device_count() -> int:
     n = C.c_int32(0)
     lib().pi2_device_count(C.byref(n))

@@ -30,12 +30,17 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// Box-Muller on the MUFU unit: r = sqrt(-2 ln u1) via lg2/sqrt.approx,
+// angle 2 pi u2 - pi in [-pi, pi) via sin/cos.approx (abs. error ~1e-6; the
+// exploration noise is specified statistically, not bitwise).
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
   const float u1 = fmaf((float)a, 2.3283064365386963e-10f, 1.1641532182693481e-10f);  // (0,1]
-  const float u2 = (float)b * 2.3283064365386963e-10f;                                   // [0,1)
-  const float r = sqrtf(-2.0f * logf(u1));
-  float s, c;
-  sincospif(2.0f * u2, &s, &c);
+  const float th = fmaf((float)b, 1.4629180792671596e-09f, -3.14159265358979f);         // [-pi,pi)
+  float lg, r, s, c;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u1));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-1.3862943611198906f * lg));  // -2 ln 2 * lg2
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
   return make_float2(r * c, r * s);
 }
 
@@ -61,7 +66,12 @@ __device__ __forceinline__ void device_eps(const StepArgs *sa, int it, uint64_t 
 // (dynamics.py:27-29; npy_divmod: fmod, then shift into the divisor's sign).
 __device__ __forceinline__ double wrap_angle(double a) {
   const double x = __dsub_rn(kPi, a);
-  double m = fmod(x, kTwoPi);
+  // fmod(x, 2pi) is x for |x| < 2pi and the exact x - 2pi on [2pi, 4pi]
+  // (Sterbenz); anything else takes the general (exact) fmod.
+  double m;
+  if (x > -kTwoPi && x < kTwoPi) m = x;
+  else if (x >= kTwoPi && x <= 2.0 * kTwoPi) m = __dsub_rn(x, kTwoPi);
+  else m = fmod(x, kTwoPi);
   if (m != 0.0) {
     if (m < 0.0) m = __dadd_rn(m, kTwoPi);
   } else {
@@ -225,9 +235,51 @@ __device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, 
   *var_out = var;
 }
 
+// Packed-pair forms: two rows per 64-bit register pair, field parameters
+// broadcast (ptxas folds make_float2(p, p) into the FFMA2 .F32 operand).
+// FFMA2 halves FMA-pipe issue slots, which lets the MUFU.EX2 of the weights
+// dispatch without starving the FMA pipe (profiles/micro/mufu_mix.cu).
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
+template <bool FULL>
+__device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *X) {
+  if (!FULL) {
+    float2 lg = __ffma2_rn(__ffma2_rn(bc(f[1]), X[0], bc(f[5])), X[0], bc(f[0]));
+    lg = __ffma2_rn(__ffma2_rn(bc(f[2]), X[1], bc(f[6])), X[1], lg);
+    lg = __ffma2_rn(__ffma2_rn(bc(f[3]), X[2], bc(f[7])), X[2], lg);
+    return __ffma2_rn(__ffma2_rn(bc(f[4]), X[3], bc(f[8])), X[3], lg);
+  } else {
+    float2 h = __ffma2_rn(bc(f[1]), X[0], bc(f[11]));
+    h = __ffma2_rn(bc(f[2]), X[1], h);
+    h = __ffma2_rn(bc(f[3]), X[2], h);
+    h = __ffma2_rn(bc(f[4]), X[3], h);
+    float2 lg = __ffma2_rn(h, X[0], bc(f[0]));
+    h = __ffma2_rn(bc(f[5]), X[1], bc(f[12]));
+    h = __ffma2_rn(bc(f[6]), X[2], h);
+    h = __ffma2_rn(bc(f[7]), X[3], h);
+    lg = __ffma2_rn(h, X[1], lg);
+    h = __ffma2_rn(bc(f[8]), X[2], bc(f[13]));
+    h = __ffma2_rn(bc(f[9]), X[3], h);
+    lg = __ffma2_rn(h, X[2], lg);
+    h = __ffma2_rn(bc(f[10]), X[3], bc(f[14]));
+    return __ffma2_rn(h, X[3], lg);
+  }
+}
+
+template <bool FULL>
+__device__ __forceinline__ float2 field_local_x2(const float *f, const float2 *X) {
+  constexpr int S = FULL ? 15 : 9;
+  float2 y = __ffma2_rn(bc(f[S + 0]), X[0], bc(f[S + 4]));
+  y = __ffma2_rn(bc(f[S + 1]), X[1], y);
+  y = __ffma2_rn(bc(f[S + 2]), X[2], y);
+  return __ffma2_rn(bc(f[S + 3]), X[3], y);
+}
+
 template <bool FULL, bool VAR, int R>
-__global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
+__global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
+  static_assert(R % 2 == 0, "rows come in pairs");
   constexpr int RS = FULL ? kRecFull : kRecDiag;
+  constexpr int P = R / 2;
   extern __shared__ float4 smem4[];
   float *srec = reinterpret_cast<float *>(smem4);
 
@@ -237,6 +289,14 @@ __global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
   for (int r = 0; r < R; ++r) {
     const int64_t row = row0 + r < a.rows ? row0 + r : a.rows - 1;
     x[r] = __ldg(a.x + row);
+  }
+  float2 X[P][4];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    X[p][0] = make_float2(x[2 * p].x, x[2 * p + 1].x);
+    X[p][1] = make_float2(x[2 * p].y, x[2 * p + 1].y);
+    X[p][2] = make_float2(x[2 * p].z, x[2 * p + 1].z);
+    X[p][3] = make_float2(x[2 * p].w, x[2 * p + 1].w);
   }
 
   if (a.resident) {
@@ -249,9 +309,9 @@ __global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
 
   for (int ax = a.a_begin; ax < a.a_end; ++ax) {
     const AxisHeader h = a.axis[ax];
-    float den[R], num[R], m2[R], lv[R];
+    float2 den[P], num[P], m2[P], lv[P];
 #pragma unroll
-    for (int r = 0; r < R; ++r) den[r] = num[r] = m2[r] = lv[r] = 0.0f;
+    for (int p = 0; p < P; ++p) den[p] = num[p] = m2[p] = lv[p] = make_float2(0.0f, 0.0f);
 
     const int tile = a.resident ? h.num_fields : a.tile;
     for (int l0 = 0; l0 < h.num_fields; l0 += tile) {
@@ -266,7 +326,7 @@ __global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
         __syncthreads();
         sp = srec;
       }
-#pragma unroll 1
+#pragma unroll 2
       for (int l = 0; l < nl; ++l) {
         float f[RS];
 #pragma unroll
@@ -275,17 +335,18 @@ __global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
           f[4 * i + 0] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
         }
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float e = ex2_ftz(field_logit2<FULL>(f, x[r]));
-          const float y = field_local<FULL>(f, x[r]);
-          den[r] += e;
+        for (int p = 0; p < P; ++p) {
+          const float2 lg = field_logit2_x2<FULL>(f, X[p]);
+          const float2 e = make_float2(ex2_ftz(lg.x), ex2_ftz(lg.y));
+          const float2 y = field_local_x2<FULL>(f, X[p]);
+          den[p] = __fadd2_rn(den[p], e);
           if (VAR) {
-            const float ey = e * y;
-            num[r] += ey;
-            m2[r] = fmaf(ey, y, m2[r]);
-            lv[r] = fmaf(e, field_lvar<FULL>(f), lv[r]);
+            const float2 ey = __fmul2_rn(e, y);
+            num[p] = __fadd2_rn(num[p], ey);
+            m2[p] = __ffma2_rn(ey, y, m2[p]);
+            lv[p] = __ffma2_rn(e, bc(field_lvar<FULL>(f)), lv[p]);
           } else {
-            num[r] = fmaf(e, y, num[r]);
+            num[p] = __ffma2_rn(e, y, num[p]);
           }
         }
       }
@@ -295,12 +356,17 @@ __global__ void __launch_bounds__(kLwprBlock) lwpr_kernel(LwprArgs a) {
     for (int r = 0; r < R; ++r) {
       const int64_t row = row0 + r;
       if (row >= a.rows) continue;
+      const int p = r / 2;
+      const float dn = (r & 1) ? den[p].y : den[p].x;
+      const float nm = (r & 1) ? num[p].y : num[p].x;
+      const float sm2 = (r & 1) ? m2[p].y : m2[p].x;
+      const float slv = (r & 1) ? lv[p].y : lv[p].x;
       const float gx = fmaf(h.gs[3], x[r].w, fmaf(h.gs[2], x[r].z, fmaf(h.gs[1], x[r].y, fmaf(h.gs[0], x[r].x, h.g0))));
       float mean, var = 0.0f;
-      if (den[r] >= kSlowDen) {
-        const float mp = __fdiv_rn(num[r], den[r]);
+      if (dn >= kSlowDen) {
+        const float mp = __fdiv_rn(nm, dn);
         mean = __fadd_rn(gx, mp);
-        if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(m2[r], lv[r]), den[r]), __fmul_rn(mp, mp)), 0.0f);
+        if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(sm2, slv), dn), __fmul_rn(mp, mp)), 0.0f);
       } else {
         lwpr_row_exact<FULL>(a.params + h.offset, h.num_fields, x[r], gx, &mean, &var);
       }
@@ -493,6 +559,142 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   double *out = a.costs + k * (int64_t)N;
   for (int t = N - 1; t >= 0; --t) {
     const double s = __dmul_rn((double)sq[t * blockDim.x + threadIdx.x], dt);
+    acc = (t == N - 1) ? s : __dadd_rn(acc, s);
+    double v = acc;
+    if (!isfinite(v)) {
+      v = ceiling;
+      crash = true;
+    }
+    out[t] = v;
+  }
+  a.crash[k] = crash ? 1 : 0;
+}
+
+// Sub-rollouts on lanes: a group of G lanes (G = S rounded up to a power of
+// two, <= 32) per rollout, lane m integrating sub-rollout m.  The M-mean is
+// the reference's pairwise tree (controller.py:314-319): for S == G an xor
+// butterfly reproduces it exactly (adjacent pairs at every level, IEEE add
+// is commutative); otherwise lane 0 replays the reference loop from shared
+// memory.  Lane 0 of the group owns the float64 suffix sum.
+template <int G>
+__global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a) {
+  constexpr int RPB = kRolloutBlock / G;  // rollouts per block
+  extern __shared__ float sq[];           // (N, RPB) stage costs
+  __shared__ float qbuf[kRolloutBlock];
+  __shared__ pi2_cost cost;
+  if (threadIdx.x == 0) cost = a.sa->cost;
+  __syncthreads();
+  const int lane_g = threadIdx.x % G, grp = threadIdx.x / G;
+  const int64_t k = (int64_t)blockIdx.x * RPB + grp;
+  const bool live = k < a.K;
+  const int S = a.M;
+  const int N = a.N;
+  const bool active = live && lane_g < S;
+  const int m = lane_g;
+  const StepArgs *sa = a.sa;
+  const float p0[3] = {__double2float_rn(sa->state[0]), __double2float_rn(sa->state[1]),
+                       __double2float_rn(sa->state[2])};
+  const float v0[3] = {__double2float_rn(sa->state[3]), __double2float_rn(sa->state[4]),
+                       __double2float_rn(sa->state[5])};
+  const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
+  const uint64_t kg = (uint64_t)(a.k_off + k);
+  const bool threshold_cost = cost.kind == PI2_COST_THRESHOLD;
+  const int64_t kk = live ? k : 0;
+
+  float cs[3] = {-0.0f, -0.0f, -0.0f}, ccs[3] = {-0.0f, -0.0f, -0.0f};
+  bool crashed = false;
+  for (int t = 0; t < N; ++t) {
+    const int64_t row = kk * (int64_t)N + t;
+    float q = 0.0f;
+    if (active) {
+      float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
+      if (a.model == PI2_MODEL_HYBRID_LWPR) {
+        const float4 m4 = a.lw_mean[row], s4 = a.lw_std[row];
+        mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
+        sd[0] = s4.x; sd[1] = s4.y; sd[2] = s4.z;
+      } else {  // two-point test model
+        mn[0] = mn[1] = mn[2] = 0.0f;
+        sd[2] = a.two_point;
+      }
+      const float4 ap = (t + 1 < N) ? a.xin[row + 1] : a.ang_last[kk];
+      const float angterm = __fmul_rn(
+          __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
+      const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
+      float d[3];
+      if (a.device_dyn) {
+        const float4 z = normals4((kg * (uint64_t)S + (uint64_t)m) * (uint64_t)N + (uint64_t)t, dk0, dk1);
+        d[0] = z.x; d[1] = z.y; d[2] = z.z;
+      } else {
+        const float *dp = a.dyn + ((kk * S + m) * (int64_t)N + t) * 3;
+        d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
+      }
+      if (a.model == PI2_MODEL_TWO_POINT) {
+        d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
+      }
+      float pos[3], vel[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float acc = __fadd_rn(__fmul_rn(sd[c], d[c]), mn[c]);
+        cs[c] = __fadd_rn(cs[c], acc);
+        ccs[c] = __fadd_rn(ccs[c], cs[c]);
+        vel[c] = __fadd_rn(__fmul_rn(cs[c], a.dp.dt32), v0[c]);
+        pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[c], cs[c]), a.dp.dt2_32), __fmul_rn(sdt, v0[c])),
+                           p0[c]);
+      }
+      if (threshold_cost) {
+        q = pos[2] > cost.threshold ? 1.0f : 0.0f;
+      } else {
+        crashed = crashed || (pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
+                  (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) || (pos[1] > cost.arena_hi[1]) ||
+                  (pos[2] > cost.arena_hi[2]);
+        q = nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed);
+      }
+    }
+    float qm;
+    if (S == G) {
+#pragma unroll
+      for (int off = 1; off < G; off <<= 1) q = __fmul_rn(0.5f, __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, off)));
+      qm = q;
+    } else {
+      qbuf[threadIdx.x] = q;
+      __syncwarp();
+      qm = 0.0f;
+      if (lane_g == 0) {
+        float v[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) v[i] = qbuf[threadIdx.x + i];
+        int n = S;
+        while (n > 1) {
+          if ((n & 1) == 0) {
+#pragma unroll
+            for (int i = 0; i < G / 2; ++i)
+              if (i < n / 2) v[i] = __fmul_rn(0.5f, __fadd_rn(v[2 * i], v[2 * i + 1]));
+            n >>= 1;
+          } else {
+            float s = v[0];
+#pragma unroll
+            for (int i = 1; i < G; ++i)
+              if (i < n) s = __fadd_rn(s, v[i]);
+            v[0] = __fdiv_rn(s, (float)n);
+            n = 1;
+          }
+        }
+        qm = v[0];
+      }
+      __syncwarp();
+    }
+    if (lane_g == 0) sq[t * RPB + grp] = qm;
+  }
+  // persistent crash of any sub-rollout (controller.py:310)
+  const unsigned ballot = __ballot_sync(0xffffffffu, crashed);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x % 32) / G * G));
+  bool crash = (ballot & gmask) != 0;
+  if (!live || lane_g != 0) return;
+  const double dt = a.dp.dt, ceiling = sa->ceiling;
+  double acc = 0.0;
+  double *out = a.costs + k * (int64_t)N;
+  for (int t = N - 1; t >= 0; --t) {
+    const double s = __dmul_rn((double)sq[t * RPB + grp], dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
     double v = acc;
     if (!isfinite(v)) {

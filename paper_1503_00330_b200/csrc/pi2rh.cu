@@ -296,19 +296,29 @@ int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   return PI2_OK;
 }
 
+template <int G>
+int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
+  auto *fn = rollout_group_kernel<G>;
+  constexpr int RPB = kRolloutBlock / G;
+  const int smem = a.N * RPB * (int)sizeof(float);
+  TRY(set_smem(ctx, fn, smem));
+  const int64_t grid = (a.K + RPB - 1) / RPB;
+  fn<<<(unsigned)grid, kRolloutBlock, smem, st>>>(a);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
 int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int S = a.spread ? a.M : 1;
-  switch (S) {
-    case 1: return launch_rollout_t<1>(ctx, a, st);
-    case 2: return launch_rollout_t<2>(ctx, a, st);
-    case 3: return launch_rollout_t<3>(ctx, a, st);
-    case 4: return launch_rollout_t<4>(ctx, a, st);
-    case 5: return launch_rollout_t<5>(ctx, a, st);
-    case 6: return launch_rollout_t<6>(ctx, a, st);
-    case 7: return launch_rollout_t<7>(ctx, a, st);
-    case 8: return launch_rollout_t<8>(ctx, a, st);
-    default: return launch_rollout_t<0>(ctx, a, st);
+  // sub-rollouts on lanes (any model but the analytic one, which is never spread)
+  if (S > 1 && S <= 32) {
+    if (S <= 2) return launch_group_t<2>(ctx, a, st);
+    if (S <= 4) return launch_group_t<4>(ctx, a, st);
+    if (S <= 8) return launch_group_t<8>(ctx, a, st);
+    if (S <= 16) return launch_group_t<16>(ctx, a, st);
+    return launch_group_t<32>(ctx, a, st);
   }
+  return S == 1 ? launch_rollout_t<1>(ctx, a, st) : launch_rollout_t<0>(ctx, a, st);
 }
 
 int check_ready(pi2_ctx *ctx) {

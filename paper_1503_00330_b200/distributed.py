@@ -92,22 +92,19 @@ class ShardedEngine:
         self.partial = torch.empty((config.horizon_steps, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=dev)
 
     def optimize(self, state, plan: ControlPlan, cost_model, cycle_index: int = 0) -> ControlPlan:
-        import torch
-
         cfg = self.config
         if cfg.iterations_per_step == 0:
             return plan
-        stream = torch.cuda.current_stream(self.device).cuda_stream
+        stream = _abi.torch_stream(self.device)
         self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
         self.ctx.call("pi2_set_cost", cost_struct(cost_model))
         args = optimize_args(cfg, cycle_index, use_graph=False)
         controls = np.ascontiguousarray(plan.controls, dtype=np.float64).copy()
         self.ctx.call("pi2_load_plan", _abi.ptr(np.ascontiguousarray(state.as_array())), _abi.ptr(controls),
-                      _abi.ptr(stream))
+                      stream)
         for it in range(cfg.iterations_per_step):
-            self.ctx.call("pi2_iterate_local", args, it, _abi.ptr(self.partial), _abi.ptr(stream))
+            self.ctx.call("pi2_iterate_local", args, it, _abi.ptr(self.partial), stream)
             gathered = gather_partials(self.partial, self.group)
-            self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, float(cfg.temperature),
-                          _abi.ptr(torch.cuda.current_stream(self.device).cuda_stream))
-        self.ctx.call("pi2_read_plan", _abi.ptr(controls), _abi.ptr(stream))
+            self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, float(cfg.temperature), stream)
+        self.ctx.call("pi2_read_plan", _abi.ptr(controls), stream)
         return plan.replaced(controls)

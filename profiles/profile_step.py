@@ -39,8 +39,6 @@ def main():
              _abi.ptr(np.ascontiguousarray(plan.controls)), None)
     import ctypes
 
-    part = np.empty((c["T"], 6))
-    dpart = ctypes.c_void_p()
     for it in range(a.iters):
         ctx.call("pi2_profile_iteration", optimize_args(cfg, it, use_graph=False), 1,
                  (ctypes.c_double * 5)())

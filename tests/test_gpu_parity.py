@@ -353,8 +353,9 @@ def test_sharded_partials_are_gpu_count_invariant():
             c.call("pi2_select_model", _abi.MODEL_HYBRID_LWPR, 0.0)
             c.call("pi2_set_dynamics", dynamics_struct(params, plan.lo, plan.hi))
             c.call("pi2_set_cost", cost_struct(cost))
-            c.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan.controls)), None)
             import torch
+
+            c.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan.controls)), None)
 
             part = torch.empty((cfg.horizon_steps, 6), dtype=torch.float64, device="cuda:0")
             c.call("pi2_iterate_local", args, 0, _abi.ptr(part), None)
