@@ -30,8 +30,10 @@ constexpr double kExpShift = 64.0;
 constexpr float kSlowDen = 1.4210854715202004e-14f;  // 2^-46
 
 // float records per receptive field in HBM/shared memory
-constexpr int kRecDiag = 16;  // 4 x float4
-constexpr int kRecFull = 24;  // 6 x float4
+constexpr int kRecDiag = 16;    // 4 x float4
+constexpr int kRecFull = 24;    // 6 x float4
+constexpr int kRecShared = 12;  // 3 x float4
+constexpr int kLayDiag = 0, kLayFull = 1, kLayShared = 2;
 
 // Host/device exact arithmetic (no contraction) for code whose rounding must
 // match on both sides.
@@ -67,6 +69,7 @@ struct DynParams {
 
 struct AxisHeader {
   float g0, gs[4];  // global linear shift g(x) = g0 + gs.x folded out of the local models
+  float qd[10];     // shared metric: log2e * (-1/2 x'Dx) coefficients (Q00 Q01 Q02 Q03 Q11 Q12 Q13 Q22 Q23 Q33)
   int num_fields;
   int64_t offset;   // float offset of the axis' first record
 };

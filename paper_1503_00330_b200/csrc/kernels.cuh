@@ -140,7 +140,7 @@ struct LwprArgs {
   const float *params;  // records of all axes (HBM)
   AxisHeader axis[3];
   int a_begin, a_end;
-  int full;             // record layout kRecFull (else kRecDiag)
+  int layout;           // kLay*
   int resident;         // all records of [a_begin, a_end) fit in shared memory
   int tile;             // fields per shared-memory tile when not resident
   int64_t rows;
@@ -157,16 +157,27 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return y;
 }
 
-template <bool FULL>
-__device__ __forceinline__ float field_logit2(const float *f, const float4 &x) {
-  if (!FULL) {
-    // f: A0, A1[4], A2[4], S[4], Y0, LV, -
+// Record layouts (floats per receptive field):
+//   kLayDiag   16: A0, A1[4], A2[4], S[4], Y0, LV, -      per-field diagonal metric
+//   kLayFull   24: A0, Q00 Q01 Q02 Q03 Q11 Q12 Q13 Q22 Q23 Q33, A2[4], S[4], Y0, LV, -
+//   kLayShared 12: A0, DC[4], S[4], Y0, LV, -             metric shared by all fields
+// A* / Q* / DC are log2(e)-scaled; with a shared metric D the quadratic
+// -1/2 x'Dx is per row (qrow, added once per field), so a field costs
+// 4 FMA + 1 ADD instead of 8 (reference LwprModel.update always copies
+// d_init into new fields, lwpr.py:208-216, so trained models share D).
+template <int LAY> struct Lay;
+template <> struct Lay<kLayDiag> { static constexpr int RS = kRecDiag, S = 9, LV = 14; };
+template <> struct Lay<kLayFull> { static constexpr int RS = kRecFull, S = 15, LV = 20; };
+template <> struct Lay<kLayShared> { static constexpr int RS = kRecShared, S = 5, LV = 10; };
+
+template <int LAY>
+__device__ __forceinline__ float field_logit2(const float *f, const float4 &x, float qrow) {
+  if (LAY == kLayDiag) {
     float lg = fmaf(fmaf(f[1], x.x, f[5]), x.x, f[0]);
     lg = fmaf(fmaf(f[2], x.y, f[6]), x.y, lg);
     lg = fmaf(fmaf(f[3], x.z, f[7]), x.z, lg);
     return fmaf(fmaf(f[4], x.w, f[8]), x.w, lg);
-  } else {
-    // f: A0, Q00 Q01 Q02 Q03, Q11 Q12 Q13, Q22 Q23, Q33, A2[4], S[4], Y0, LV
+  } else if (LAY == kLayFull) {
     float h = fmaf(f[1], x.x, f[11]);
     h = fmaf(f[2], x.y, h);
     h = fmaf(f[3], x.z, h);
@@ -181,21 +192,36 @@ __device__ __forceinline__ float field_logit2(const float *f, const float4 &x) {
     lg = fmaf(h, x.z, lg);
     h = fmaf(f[10], x.w, f[14]);
     return fmaf(h, x.w, lg);
+  } else {
+    const float lg = fmaf(f[4], x.w, fmaf(f[3], x.z, fmaf(f[2], x.y, fmaf(f[1], x.x, f[0]))));
+    return __fadd_rn(lg, qrow);
   }
 }
 
-template <bool FULL>
+template <int LAY>
 __device__ __forceinline__ float field_local(const float *f, const float4 &x) {
-  constexpr int S = FULL ? 15 : 9;
+  constexpr int S = Lay<LAY>::S;
   float y = fmaf(f[S + 0], x.x, f[S + 4]);
   y = fmaf(f[S + 1], x.y, y);
   y = fmaf(f[S + 2], x.z, y);
   return fmaf(f[S + 3], x.w, y);
 }
 
-template <bool FULL>
+template <int LAY>
 __device__ __forceinline__ float field_lvar(const float *f) {
-  return f[FULL ? 20 : 14];
+  return f[Lay<LAY>::LV];
+}
+
+// per-row log2-scaled quadratic of a shared metric, plus the 2^64 shift
+__device__ __forceinline__ float shared_qrow(const AxisHeader &h, const float4 &x) {
+  float r = fmaf(h.qd[0], x.x, fmaf(h.qd[1], x.y, fmaf(h.qd[2], x.z, h.qd[3] * x.w)));
+  float q = r * x.x;
+  r = fmaf(h.qd[4], x.y, fmaf(h.qd[5], x.z, h.qd[6] * x.w));
+  q = fmaf(r, x.y, q);
+  r = fmaf(h.qd[7], x.z, h.qd[8] * x.w);
+  q = fmaf(r, x.z, q);
+  q = fmaf(h.qd[9] * x.w, x.w, q);
+  return __fadd_rn(q, (float)kExpShift);
 }
 
 // Reference-exact evaluation of one row (rare: every weight is (nearly)
@@ -203,33 +229,33 @@ __device__ __forceinline__ float field_lvar(const float *f) {
 // rounding (here scaled by 2^64: multiples of 2^-85 below 2^-62), w = e/den
 // (0/0 = NaN -> cost ceiling downstream), mean = sum w y, two-pass variance
 // (lwpr.py:395-407).
-template <bool FULL>
-__device__ __forceinline__ float exact_weight(const float *f, const float4 &x) {
-  float e = exp2f(field_logit2<FULL>(f, x));  // IEEE exp2f: never flushes
+template <int LAY>
+__device__ __forceinline__ float exact_weight(const float *f, const float4 &x, float qrow) {
+  float e = exp2f(field_logit2<LAY>(f, x, qrow));  // IEEE exp2f: never flushes
   // float32 denormal grid of exp(q) (step 2^-149), in 2^64-scaled units:
   // multiples of 2^-85 below 2^-62 (exact products by powers of two)
   if (e < 2.168404344971009e-19f) e = rintf(e * 3.8685626227668134e25f) * 2.5849394142282115e-26f;
   return e;
 }
 
-template <bool FULL>
-__device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, float gx,
+template <int LAY>
+__device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, float qrow, float gx,
                                             float *mean_out, float *var_out) {
-  constexpr int RS = FULL ? kRecFull : kRecDiag;
+  constexpr int RS = Lay<LAY>::RS;
   float den = 0.0f;
-  for (int l = 0; l < nf; ++l) den = __fadd_rn(den, exact_weight<FULL>(rec + (int64_t)l * RS, x));
+  for (int l = 0; l < nf; ++l) den = __fadd_rn(den, exact_weight<LAY>(rec + (int64_t)l * RS, x, qrow));
   float mean = 0.0f;
   for (int l = 0; l < nf; ++l) {
     const float *f = rec + (int64_t)l * RS;
-    const float w = __fdiv_rn(exact_weight<FULL>(f, x), den);
-    mean = __fadd_rn(mean, __fmul_rn(w, __fadd_rn(field_local<FULL>(f, x), gx)));
+    const float w = __fdiv_rn(exact_weight<LAY>(f, x, qrow), den);
+    mean = __fadd_rn(mean, __fmul_rn(w, __fadd_rn(field_local<LAY>(f, x), gx)));
   }
   float var = 0.0f;
   for (int l = 0; l < nf; ++l) {
     const float *f = rec + (int64_t)l * RS;
-    const float w = __fdiv_rn(exact_weight<FULL>(f, x), den);
-    const float d = __fsub_rn(mean, __fadd_rn(field_local<FULL>(f, x), gx));
-    var = __fadd_rn(var, __fmul_rn(w, __fadd_rn(__fmul_rn(d, d), field_lvar<FULL>(f))));
+    const float w = __fdiv_rn(exact_weight<LAY>(f, x, qrow), den);
+    const float d = __fsub_rn(mean, __fadd_rn(field_local<LAY>(f, x), gx));
+    var = __fadd_rn(var, __fmul_rn(w, __fadd_rn(__fmul_rn(d, d), field_lvar<LAY>(f))));
   }
   *mean_out = mean;
   *var_out = var;
@@ -241,14 +267,14 @@ __device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, 
 // dispatch without starving the FMA pipe (profiles/micro/mufu_mix.cu).
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-template <bool FULL>
-__device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *X) {
-  if (!FULL) {
+template <int LAY>
+__device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *X, float2 Q) {
+  if (LAY == kLayDiag) {
     float2 lg = __ffma2_rn(__ffma2_rn(bc(f[1]), X[0], bc(f[5])), X[0], bc(f[0]));
     lg = __ffma2_rn(__ffma2_rn(bc(f[2]), X[1], bc(f[6])), X[1], lg);
     lg = __ffma2_rn(__ffma2_rn(bc(f[3]), X[2], bc(f[7])), X[2], lg);
     return __ffma2_rn(__ffma2_rn(bc(f[4]), X[3], bc(f[8])), X[3], lg);
-  } else {
+  } else if (LAY == kLayFull) {
     float2 h = __ffma2_rn(bc(f[1]), X[0], bc(f[11]));
     h = __ffma2_rn(bc(f[2]), X[1], h);
     h = __ffma2_rn(bc(f[3]), X[2], h);
@@ -263,22 +289,28 @@ __device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *
     lg = __ffma2_rn(h, X[2], lg);
     h = __ffma2_rn(bc(f[10]), X[3], bc(f[14]));
     return __ffma2_rn(h, X[3], lg);
+  } else {
+    float2 lg = __ffma2_rn(bc(f[1]), X[0], bc(f[0]));
+    lg = __ffma2_rn(bc(f[2]), X[1], lg);
+    lg = __ffma2_rn(bc(f[3]), X[2], lg);
+    lg = __ffma2_rn(bc(f[4]), X[3], lg);
+    return __fadd2_rn(lg, Q);
   }
 }
 
-template <bool FULL>
+template <int LAY>
 __device__ __forceinline__ float2 field_local_x2(const float *f, const float2 *X) {
-  constexpr int S = FULL ? 15 : 9;
+  constexpr int S = Lay<LAY>::S;
   float2 y = __ffma2_rn(bc(f[S + 0]), X[0], bc(f[S + 4]));
   y = __ffma2_rn(bc(f[S + 1]), X[1], y);
   y = __ffma2_rn(bc(f[S + 2]), X[2], y);
   return __ffma2_rn(bc(f[S + 3]), X[3], y);
 }
 
-template <bool FULL, bool VAR, int R>
-__global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
+template <int LAY, bool VAR, int R, int BLOCK = kLwprBlock, int MINB = 4>
+__global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
   static_assert(R % 2 == 0, "rows come in pairs");
-  constexpr int RS = FULL ? kRecFull : kRecDiag;
+  constexpr int RS = Lay<LAY>::RS;
   constexpr int P = R / 2;
   extern __shared__ float4 smem4[];
   float *srec = reinterpret_cast<float *>(smem4);
@@ -309,9 +341,13 @@ __global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
 
   for (int ax = a.a_begin; ax < a.a_end; ++ax) {
     const AxisHeader h = a.axis[ax];
-    float2 den[P], num[P], m2[P], lv[P];
+    float2 den[P], num[P], m2[P], lv[P], Q[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) den[p] = num[p] = m2[p] = lv[p] = make_float2(0.0f, 0.0f);
+    for (int p = 0; p < P; ++p) {
+      den[p] = num[p] = m2[p] = lv[p] = make_float2(0.0f, 0.0f);
+      Q[p] = LAY == kLayShared ? make_float2(shared_qrow(h, x[2 * p]), shared_qrow(h, x[2 * p + 1]))
+                               : make_float2(0.0f, 0.0f);
+    }
 
     const int tile = a.resident ? h.num_fields : a.tile;
     for (int l0 = 0; l0 < h.num_fields; l0 += tile) {
@@ -336,15 +372,15 @@ __global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-          const float2 lg = field_logit2_x2<FULL>(f, X[p]);
+          const float2 lg = field_logit2_x2<LAY>(f, X[p], Q[p]);
           const float2 e = make_float2(ex2_ftz(lg.x), ex2_ftz(lg.y));
-          const float2 y = field_local_x2<FULL>(f, X[p]);
+          const float2 y = field_local_x2<LAY>(f, X[p]);
           den[p] = __fadd2_rn(den[p], e);
           if (VAR) {
             const float2 ey = __fmul2_rn(e, y);
             num[p] = __fadd2_rn(num[p], ey);
             m2[p] = __ffma2_rn(ey, y, m2[p]);
-            lv[p] = __ffma2_rn(e, bc(field_lvar<FULL>(f)), lv[p]);
+            lv[p] = __ffma2_rn(e, bc(field_lvar<LAY>(f)), lv[p]);
           } else {
             num[p] = __ffma2_rn(e, y, num[p]);
           }
@@ -361,6 +397,7 @@ __global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
       const float nm = (r & 1) ? num[p].y : num[p].x;
       const float sm2 = (r & 1) ? m2[p].y : m2[p].x;
       const float slv = (r & 1) ? lv[p].y : lv[p].x;
+      const float qr = (r & 1) ? Q[p].y : Q[p].x;
       const float gx = fmaf(h.gs[3], x[r].w, fmaf(h.gs[2], x[r].z, fmaf(h.gs[1], x[r].y, fmaf(h.gs[0], x[r].x, h.g0))));
       float mean, var = 0.0f;
       if (dn >= kSlowDen) {
@@ -368,7 +405,7 @@ __global__ void __launch_bounds__(kLwprBlock, 4) lwpr_kernel(LwprArgs a) {
         mean = __fadd_rn(gx, mp);
         if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(sm2, slv), dn), __fmul_rn(mp, mp)), 0.0f);
       } else {
-        lwpr_row_exact<FULL>(a.params + h.offset, h.num_fields, x[r], gx, &mean, &var);
+        lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, x[r], qr, gx, &mean, &var);
       }
       const int64_t o = row * a.out_stride + (ax - a.a_begin);
       a.mean_out[o] = mean;

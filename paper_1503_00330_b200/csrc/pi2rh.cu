@@ -16,14 +16,10 @@
 #include <string>
 #include <vector>
 
+#include "fold.h"
 #include "kernels.cuh"
 
 using namespace pi2;
-
-struct AxisRaw {
-  int L = 0, d = 0;
-  std::vector<double> centers, metrics, coefs, lvar;
-};
 
 struct pi2_ctx {
   int device = 0;
@@ -44,7 +40,7 @@ struct pi2_ctx {
   double model_param = 0.0;
   AxisRaw axes[3];
   bool params_dirty = true;
-  bool params_full = false;
+  int layout = kLayDiag;
   AxisHeader hdr[3]{};
   float *d_params = nullptr;
   size_t params_cap = 0;
@@ -128,91 +124,19 @@ void invalidate_graph(pi2_ctx *ctx) {
   ctx->graph_iters = -1;
 }
 
-// ---- FrozenLwpr folding (lwpr.py:339-358), float64, padded to 4 inputs ----
-bool axis_is_diagonal(const AxisRaw &a) {
-  for (int l = 0; l < a.L; ++l)
-    for (int i = 0; i < a.d; ++i)
-      for (int j = 0; j < a.d; ++j)
-        if (i != j && a.metrics[((size_t)l * a.d + i) * a.d + j] != 0.0) return false;
-  return true;
-}
-
-void fold_axis(const AxisRaw &a, bool full, std::vector<float> &rec, AxisHeader &h) {
-  const int RS = full ? kRecFull : kRecDiag;
-  const size_t base = rec.size();
-  rec.resize(base + (size_t)a.L * RS, 0.0f);
-  std::vector<double> y0(a.L), s(4 * (size_t)a.L, 0.0);
-  double g0 = 0.0, gs[4] = {0, 0, 0, 0};
-  for (int l = 0; l < a.L; ++l) {
-    double yy = a.coefs[(size_t)l * (a.d + 1)];
-    for (int i = 0; i < a.d; ++i) {
-      const double si = a.coefs[(size_t)l * (a.d + 1) + 1 + i];
-      s[4 * (size_t)l + i] = si;
-      yy -= si * a.centers[(size_t)l * a.d + i];  // y0 = coef0 - s.c (lwpr.py:355-357)
-    }
-    y0[l] = yy;
-    g0 += yy;
-    for (int i = 0; i < 4; ++i) gs[i] += s[4 * (size_t)l + i];
-  }
-  g0 /= a.L;
-  for (double &v : gs) v /= a.L;
-  h.g0 = (float)g0;
-  for (int i = 0; i < 4; ++i) h.gs[i] = (float)gs[i];
-  h.num_fields = a.L;
-  h.offset = (int64_t)base;
-  for (int l = 0; l < a.L; ++l) {
-    double c[4] = {0, 0, 0, 0}, D[4][4] = {{0}};
-    for (int i = 0; i < a.d; ++i) {
-      c[i] = a.centers[(size_t)l * a.d + i];
-      for (int j = 0; j < a.d; ++j) D[i][j] = a.metrics[((size_t)l * a.d + i) * a.d + j];
-    }
-    double dc[4], a0 = 0.0;
-    for (int i = 0; i < 4; ++i) {  // dc = D c (lwpr.py:344)
-      dc[i] = 0.0;
-      for (int j = 0; j < 4; ++j) dc[i] += D[i][j] * c[j];
-    }
-    for (int i = 0; i < 4; ++i) a0 += dc[i] * c[i];
-    a0 *= -0.5;  // lwpr.py:347
-    float *f = rec.data() + base + (size_t)l * RS;
-    f[0] = (float)(a0 * kLog2e + kExpShift);
-    if (!full) {
-      for (int i = 0; i < 4; ++i) {
-        f[1 + i] = (float)(-0.5 * D[i][i] * kLog2e);  // a1 (lwpr.py:345)
-        f[5 + i] = (float)(dc[i] * kLog2e);           // a2 (lwpr.py:346)
-        f[9 + i] = (float)(s[4 * (size_t)l + i] - gs[i]);
-      }
-      f[13] = (float)(y0[l] - g0);
-      f[14] = (float)a.lvar[l];
-    } else {
-      int q = 1;
-      for (int i = 0; i < 4; ++i)
-        for (int j = i; j < 4; ++j)
-          f[q++] = (float)((i == j ? -0.5 * D[i][i] : -0.5 * (D[i][j] + D[j][i])) * kLog2e);
-      for (int i = 0; i < 4; ++i) {
-        f[11 + i] = (float)(dc[i] * kLog2e);
-        f[15 + i] = (float)(s[4 * (size_t)l + i] - gs[i]);
-      }
-      f[19] = (float)(y0[l] - g0);
-      f[20] = (float)a.lvar[l];
-    }
-  }
-}
-
 int ensure_params(pi2_ctx *ctx) {
   if (!ctx->params_dirty) return PI2_OK;
-  bool full = false;
-  for (auto &a : ctx->axes)
-    if (a.L > 0 && !axis_is_diagonal(a)) full = true;
+  const int layout = choose_layout(ctx->axes, 3);
   std::vector<float> rec;
   for (int ax = 0; ax < 3; ++ax) {
-    if (ctx->axes[ax].L > 0) fold_axis(ctx->axes[ax], full, rec, ctx->hdr[ax]);
+    if (ctx->axes[ax].L > 0) fold_axis(ctx->axes[ax], layout, rec, ctx->hdr[ax]);
     else ctx->hdr[ax] = AxisHeader{};
   }
   if (!rec.empty()) {
     TRY(ensure(ctx, (void **)&ctx->d_params, &ctx->params_cap, rec.size() * sizeof(float)));
     CU(cudaMemcpy(ctx->d_params, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
-  ctx->params_full = full;
+  ctx->layout = layout;
   ctx->params_dirty = false;
   return PI2_OK;
 }
@@ -226,9 +150,9 @@ int set_smem(pi2_ctx *ctx, F *fn, int bytes) {
 
 int lwpr_smem_limit(pi2_ctx *ctx) { return std::min(ctx->smem_optin, 64 * 1024); }
 
-template <bool FULL, bool VAR, int R>
+template <int LAY, bool VAR, int R>
 int launch_lwpr_t(pi2_ctx *ctx, const LwprArgs &a, int smem, cudaStream_t st) {
-  auto *fn = lwpr_kernel<FULL, VAR, R>;
+  auto *fn = lwpr_kernel<LAY, VAR, R>;
   TRY(set_smem(ctx, fn, smem));
   const int64_t per_block = (int64_t)kLwprBlock * R;
   const int64_t grid = (a.rows + per_block - 1) / per_block;
@@ -245,8 +169,8 @@ int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4
   for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
   a.a_begin = a_begin;
   a.a_end = a_end;
-  a.full = ctx->params_full;
-  const int RS = ctx->params_full ? kRecFull : kRecDiag;
+  a.layout = ctx->layout;
+  const int RS = record_floats(ctx->layout);
   int64_t fields = 0, maxL = 0;
   for (int ax = a_begin; ax < a_end; ++ax) {
     fields += ctx->hdr[ax].num_fields;
@@ -272,12 +196,18 @@ int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4
   a.sqrt_out = sqrt_out;
   const bool var = sd_out != nullptr;
   const bool small = rows < (int64_t)2 * 148 * kLwprBlock * kLwprRows;
-  if (ctx->params_full) {
-    if (var) return small ? launch_lwpr_t<true, true, 2>(ctx, a, smem, st) : launch_lwpr_t<true, true, kLwprRows>(ctx, a, smem, st);
-    return small ? launch_lwpr_t<true, false, 2>(ctx, a, smem, st) : launch_lwpr_t<true, false, kLwprRows>(ctx, a, smem, st);
+#define PI2_LWPR_CASE(LAY)                                                                          \
+  if (ctx->layout == LAY) {                                                                         \
+    if (var) return small ? launch_lwpr_t<LAY, true, 2>(ctx, a, smem, st)                           \
+                          : launch_lwpr_t<LAY, true, kLwprRows>(ctx, a, smem, st);                  \
+    return small ? launch_lwpr_t<LAY, false, 2>(ctx, a, smem, st)                                   \
+                 : launch_lwpr_t<LAY, false, kLwprRows>(ctx, a, smem, st);                          \
   }
-  if (var) return small ? launch_lwpr_t<false, true, 2>(ctx, a, smem, st) : launch_lwpr_t<false, true, kLwprRows>(ctx, a, smem, st);
-  return small ? launch_lwpr_t<false, false, 2>(ctx, a, smem, st) : launch_lwpr_t<false, false, kLwprRows>(ctx, a, smem, st);
+  PI2_LWPR_CASE(kLayShared)
+  PI2_LWPR_CASE(kLayDiag)
+  PI2_LWPR_CASE(kLayFull)
+#undef PI2_LWPR_CASE
+  return fail(ctx, PI2_ERR_STATE, "unknown LWPR layout %d", ctx->layout);
 }
 
 bool spread(const pi2_ctx *ctx) {
