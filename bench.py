@@ -248,9 +248,12 @@ def run_ours(args, rank: int, world: int, local: int):
     partial = torch.empty((T, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=f"cuda:{local}")
 
     def device_step(cycle):
+        if world == 1:  # the whole iteration as one CUDA graph on the device-resident plan
+            ctx.call("pi2_iterate_device", optimize_args(cfg, cycle, use_graph=True), sptr)
+            return
         a = optimize_args(cfg, cycle, use_graph=False)
         ctx.call("pi2_iterate_local", a, 0, _abi.ptr(partial), sptr)
-        g = gather_partials(partial) if world > 1 else partial
+        g = gather_partials(partial)
         ctx.call("pi2_iterate_finalize", _abi.ptr(g), world, float(cfg.temperature), sptr)
 
     def barrier():
@@ -369,7 +372,7 @@ def run_ours(args, rank: int, world: int, local: int):
         },
         "stages_ms": stages,
         "clocks": clk,
-        "gpu_launches": args.steps * (KERNELS_PER_ITER + 1),
+        "gpu_launches": args.steps * (KERNELS_PER_ITER + (1 if world > 1 else 0)),
     }
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(cfgd, args.cpu_sample, args.cpu_seconds)

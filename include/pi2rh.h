@@ -160,6 +160,10 @@ int pi2_update_device(pi2_ctx *ctx, int64_t num_rollouts, int32_t horizon_steps,
  * splitmix64 stream address, rng.py:33-44).  plan_inout (N,4) HOST. */
 int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout,
                  const pi2_optimize_args *args);
+/* The optimise loop on the device-resident plan (set by pi2_load_plan, read
+ * back by pi2_read_plan): no host transfers or synchronisation, replayed as
+ * one CUDA graph when args->use_graph. */
+int pi2_iterate_device(pi2_ctx *ctx, const pi2_optimize_args *args, void *stream);
 /* receding_horizon_step (controller.py:398-413): optimize, return the first
  * control (4,) and replace plan_inout by the shifted plan (:63-66). */
 int pi2_receding_horizon_step(pi2_ctx *ctx, const double *state, double *plan_inout,

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "pi2_update": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_double, _P]),
     "pi2_update_device": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_double, _P, _P]),
     "pi2_optimize": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs)]),
+    "pi2_iterate_device": (C.c_int, [_P, C.POINTER(OptimizeArgs), _P]),
     "pi2_receding_horizon_step": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs), _P]),
     "pi2_load_plan": (C.c_int, [_P, _P, _P, _P]),
     "pi2_read_plan": (C.c_int, [_P, _P, _P]),

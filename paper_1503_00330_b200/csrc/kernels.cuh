@@ -99,30 +99,40 @@ __global__ void __launch_bounds__(kRolloutBlock)
   double rate[3] = {sa->state[9], sa->state[10], sa->state[11]};
   const double *ek = DEVICE_NOISE ? nullptr : eps + k * (int64_t)N * 4;
   float4 *xk = xin + k * (int64_t)N;
-  for (int t = 0; t < N; ++t) {
-    double e[4];
-    if (DEVICE_NOISE) {
-      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
-      if (eps_out) {
-        double2 *o = reinterpret_cast<double2 *>(eps_out + (k * (int64_t)N + t) * 4);
-        o[0] = make_double2(e[0], e[1]);
-        o[1] = make_double2(e[2], e[3]);
+  constexpr int TB = 4;  // noise of TB steps is generated before their serial FP64 recurrence
+  for (int t0 = 0; t0 < N; t0 += TB) {
+    double e[TB][4];
+#pragma unroll
+    for (int j = 0; j < TB; ++j) {
+      const int t = t0 + j < N ? t0 + j : N - 1;
+      if (DEVICE_NOISE) {
+        device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e[j]);
+      } else {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
+        const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
+        e[j][0] = a.x; e[j][1] = a.y; e[j][2] = b.x; e[j][3] = b.y;
       }
-    } else {
-      const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
-      const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
-      e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
     }
-    double u[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      u[c] = fmin(fmax(__dadd_rn(splan[4 * t + c], e[c]), dp.lo[c]), dp.hi[c]);
-    xk[t] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
-                        __double2float_rn(ang[2]), __double2float_rn(u[3]));
+    for (int j = 0; j < TB; ++j) {
+      const int t = t0 + j;
+      if (t >= N) break;
+      if (DEVICE_NOISE && eps_out) {
+        double2 *o = reinterpret_cast<double2 *>(eps_out + (k * (int64_t)N + t) * 4);
+        o[0] = make_double2(e[j][0], e[j][1]);
+        o[1] = make_double2(e[j][2], e[j][3]);
+      }
+      double u[4];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      ang[c] = wrap_angle(__dadd_rn(ang[c], __dmul_rn(rate[c], dp.dt)));
-      rate[c] = __dadd_rn(rate[c], __dmul_rn(dp.gain_dt, __dsub_rn(u[c], rate[c])));
+      for (int c = 0; c < 4; ++c)
+        u[c] = fmin(fmax(__dadd_rn(splan[4 * t + c], e[j][c]), dp.lo[c]), dp.hi[c]);
+      xk[t] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
+                          __double2float_rn(ang[2]), __double2float_rn(u[3]));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        ang[c] = wrap_angle(__dadd_rn(ang[c], __dmul_rn(rate[c], dp.dt)));
+        rate[c] = __dadd_rn(rate[c], __dmul_rn(dp.gain_dt, __dsub_rn(u[c], rate[c])));
+      }
     }
   }
   ang_last[k] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
@@ -640,20 +650,36 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
 
   float cs[3] = {-0.0f, -0.0f, -0.0f}, ccs[3] = {-0.0f, -0.0f, -0.0f};
   bool crashed = false;
+  const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
+  // rows of step t+1 are loaded while step t computes (hides HBM latency)
+  float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n, apn = m4n;
+  if (active) {
+    if (hybrid) {
+      m4n = __ldg(a.lw_mean + kk * (int64_t)N);
+      s4n = __ldg(a.lw_std + kk * (int64_t)N);
+    }
+    apn = (1 < N) ? __ldg(a.xin + kk * (int64_t)N + 1) : __ldg(a.ang_last + kk);
+  }
   for (int t = 0; t < N; ++t) {
     const int64_t row = kk * (int64_t)N + t;
+    const float4 m4 = m4n, s4 = s4n, ap = apn;
+    if (active && t + 1 < N) {
+      if (hybrid) {
+        m4n = __ldg(a.lw_mean + row + 1);
+        s4n = __ldg(a.lw_std + row + 1);
+      }
+      apn = (t + 2 < N) ? __ldg(a.xin + row + 2) : __ldg(a.ang_last + kk);
+    }
     float q = 0.0f;
     if (active) {
       float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
-      if (a.model == PI2_MODEL_HYBRID_LWPR) {
-        const float4 m4 = a.lw_mean[row], s4 = a.lw_std[row];
+      if (hybrid) {
         mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
         sd[0] = s4.x; sd[1] = s4.y; sd[2] = s4.z;
       } else {  // two-point test model
         mn[0] = mn[1] = mn[2] = 0.0f;
         sd[2] = a.two_point;
       }
-      const float4 ap = (t + 1 < N) ? a.xin[row + 1] : a.ang_last[kk];
       const float angterm = __fmul_rn(
           __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
       const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
@@ -766,43 +792,54 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
                     double neg_inv, double *__restrict__ out) {
   constexpr int J = kChunk / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.y * kChunkWarps + warp;  // one warp per (chunk, t)
+  if (t >= N) return;
   const int64_t k0 = (int64_t)blockIdx.x * kChunk;
-  for (int t = warp; t < N; t += kChunkWarps) {
-    double s[J];
-    double m = INFINITY;
+  double s[J];
+  double m = INFINITY;
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int64_t k = k0 + lane + 32 * j;
-      s[j] = k < K ? costs[k * N + t] : INFINITY;
-      m = fmin(m, s[j]);
-    }
-    m = warp_min(m);
-    double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int64_t k = k0 + lane + 32 * j;
-      if (k >= K) continue;
-      const double w = exp(__dmul_rn(__dsub_rn(s[j], m), neg_inv));
-      double e[4];
-      if (eps) {
-        const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
-        const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
-        e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
-      } else {
-        device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
-      }
-      z = __dadd_rn(z, w);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[c] = __dadd_rn(v[c], __dmul_rn(w, e[c]));
-    }
-    z = warp_sum(z);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = warp_sum(v[c]);
-    if (lane == 0) {
-      double *o = out + ((int64_t)blockIdx.x * N + t) * PI2_PARTIAL_WIDTH;
-      o[0] = m; o[1] = z; o[2] = v[0]; o[3] = v[1]; o[4] = v[2]; o[5] = v[3];
-    }
+  for (int j = 0; j < J; ++j) {
+    const int64_t k = k0 + lane + 32 * j;
+    s[j] = k < K ? __ldg(costs + k * N + t) : INFINITY;
+    m = fmin(m, s[j]);
   }
+  m = warp_min(m);
+  double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int64_t k = k0 + lane + 32 * j;
+    if (k >= K) continue;
+    const double w = exp(__dmul_rn(__dsub_rn(s[j], m), neg_inv));
+    double e[4];
+    if (eps) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
+      e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    } else {
+      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+    }
+    z = __dadd_rn(z, w);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __dadd_rn(v[c], __dmul_rn(w, e[c]));
+  }
+  z = warp_sum(z);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = warp_sum(v[c]);
+  if (lane == 0) {
+    double *o = out + ((int64_t)blockIdx.x * N + t) * PI2_PARTIAL_WIDTH;
+    o[0] = m; o[1] = z; o[2] = v[0]; o[3] = v[1]; o[4] = v[2]; o[5] = v[3];
+  }
+}
+
+// plan[t] += V/Z of a single partial, clipped (the world-size-1 finalize)
+__global__ void apply_root_kernel(const double *__restrict__ root, int N, double *__restrict__ plan,
+                                  DynParams dp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 4 * N) return;
+  const int t = i / 4, c = i % 4;
+  const double *r = root + t * PI2_PARTIAL_WIDTH;
+  const double du = __ddiv_rn(r[2 + c], r[1]);
+  plan[i] = fmin(fmax(__dadd_rn(plan[i], du), dp.lo[c]), dp.hi[c]);
 }
 
 // ---------------------------------------------------------------------------

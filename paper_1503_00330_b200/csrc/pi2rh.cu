@@ -337,8 +337,17 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   return launch_rollout(ctx, a, st);
 }
 
+dim3 partials_grid(int64_t chunks, int N) {
+  return dim3((unsigned)chunks, (unsigned)((N + kChunkWarps - 1) / kChunkWarps));
+}
+
 int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
                    double *plan, cudaStream_t st) {
+  if (n == 1 && !root && plan) {  // a single partial: just apply it
+    apply_root_kernel<<<(4 * N + 127) / 128, 128, 0, st>>>(leaves, N, plan, ctx->dp);
+    CU(cudaGetLastError());
+    return PI2_OK;
+  }
   if ((n + kSeg - 1) / kSeg > kSeg) return fail(ctx, PI2_ERR_INVALID, "too many partials (%lld)", (long long)n);
   const int smem = 2 * kSeg * PI2_PARTIAL_WIDTH * (int)sizeof(double);
   TRY(set_smem(ctx, combine_kernel, smem));
@@ -351,7 +360,7 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
                      cudaStream_t st) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
-  partials_kernel<<<(unsigned)ctx->n_chunks, 32 * kChunkWarps, 0, st>>>(
+  partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
       ctx->d_costs, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
       ctx->d_partials);
   CU(cudaGetLastError());
@@ -627,8 +636,8 @@ int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, co
   double *dplan = partials + PI2_PARTIAL_WIDTH * chunks * N;
   CU(cudaMemcpyAsync(dplan, plan, plbytes, cudaMemcpyHostToDevice, st));
   const double neg_inv = -1.0 / temperature;
-  partials_kernel<<<(unsigned)chunks, 32 * kChunkWarps, 0, st>>>(costs_dev, noise_dev, ctx->d_args, 0, K, 0,
-                                                                  N, neg_inv, partials);
+  partials_kernel<<<partials_grid(chunks, N), 32 * kChunkWarps, 0, st>>>(costs_dev, noise_dev, ctx->d_args, 0,
+                                                                         K, 0, N, neg_inv, partials);
   CU(cudaGetLastError());
   TRY(launch_combine(ctx, partials, chunks, N, neg_inv, nullptr, dplan, st));
   CU(cudaMemcpyAsync(plan_out, dplan, plbytes, cudaMemcpyDeviceToHost, st));
@@ -649,6 +658,50 @@ int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const dou
   return pi2_update_device(ctx, K, N, plan, dcosts, dnoise, temperature, plan_out, st);
 }
 
+// All iterations of a step on the device plan: eager, or one cached CUDA graph
+// (kernel arguments are fixed pointers; per-call state, keys and cost come
+// from the staged StepArgs, so replays need no re-capture).
+static int run_iterations(pi2_ctx *ctx, const pi2_optimize_args *args, cudaStream_t st) {
+  const double neg_inv = -1.0 / args->temperature;
+  if (!args->use_graph) {
+    for (int it = 0; it < args->iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
+    return PI2_OK;
+  }
+  if (!(ctx->graph && ctx->graph_iters == args->iterations && ctx->graph_neg_inv == neg_inv)) {
+    invalidate_graph(ctx);
+    // capture on the private stream (never a caller's), ordered after `st` by the launch below
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = PI2_OK;
+    for (int it = 0; it < args->iterations && rc == PI2_OK; ++it)
+      rc = launch_iteration(ctx, it, neg_inv, nullptr, true, ctx->stream);
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc != PI2_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ec != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&ctx->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+    ctx->graph_iters = args->iterations;
+    ctx->graph_neg_inv = neg_inv;
+  }
+  CU(cudaGraphLaunch(ctx->graph, st));
+  return PI2_OK;
+}
+
+int pi2_iterate_device(pi2_ctx *ctx, const pi2_optimize_args *args, void *stream) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (args->iterations == 0) return PI2_OK;
+  cudaStream_t st = pick(ctx, stream);
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, nullptr, args, args->cost_ceiling, st));
+  return run_iterations(ctx, args, st);
+}
+
 int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi2_optimize_args *args) {
   TRY(check_ready(ctx));
   TRY(bind(ctx));
@@ -658,42 +711,10 @@ int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi
   cudaStream_t st = ctx->stream;
   TRY(ensure_params(ctx));
   TRY(stage_args(ctx, state, args, args->cost_ceiling, st));
-  const double neg_inv = -1.0 / args->temperature;
   std::memcpy(ctx->h_plan, plan_inout, sizeof(double) * 4 * ctx->N);
-  // temperature is baked into the graph's kernel arguments
-  if (args->use_graph && ctx->graph && ctx->graph_iters == args->iterations &&
-      ctx->graph_neg_inv == neg_inv) {
-    CU(cudaGraphLaunch(ctx->graph, st));
-  } else {
-    invalidate_graph(ctx);
-    auto body = [&]() -> int {
-      CU(cudaMemcpyAsync(ctx->d_plan, ctx->h_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyHostToDevice, st));
-      for (int it = 0; it < args->iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
-      CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost, st));
-      return PI2_OK;
-    };
-    if (args->use_graph) {
-      // kernel attributes must be set before capture
-      cudaGraph_t g = nullptr;
-      CU(cudaStreamSynchronize(st));
-      CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      const int rc = body();
-      const cudaError_t ec = cudaStreamEndCapture(st, &g);
-      if (rc != PI2_OK) {
-        if (g) cudaGraphDestroy(g);
-        return rc;
-      }
-      if (ec != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
-      const cudaError_t ei = cudaGraphInstantiate(&ctx->graph, g, 0);
-      cudaGraphDestroy(g);
-      if (ei != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
-      ctx->graph_iters = args->iterations;
-      ctx->graph_neg_inv = neg_inv;
-      CU(cudaGraphLaunch(ctx->graph, st));
-    } else {
-      TRY(body());
-    }
-  }
+  CU(cudaMemcpyAsync(ctx->d_plan, ctx->h_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyHostToDevice, st));
+  TRY(run_iterations(ctx, args, st));
+  CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   std::memcpy(plan_inout, ctx->h_plan, sizeof(double) * 4 * ctx->N);
   return PI2_OK;
@@ -758,7 +779,7 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
     rc = launch_rollouts(ctx, 0, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, ev);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[3], st);
-    partials_kernel<<<(unsigned)ctx->n_chunks, 32 * kChunkWarps, 0, st>>>(
+    partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
         ctx->d_costs, nullptr, ctx->d_args, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
         ctx->d_partials);
     cudaEventRecord(ev[4], st);
