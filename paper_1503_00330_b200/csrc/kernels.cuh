@@ -6,8 +6,10 @@
 //   partials_kernel  K11a:  per-chunk (min, Z, V) softmax partials
 //   combine_kernel   K11b:  fixed-order tree combine + plan update
 //
-// Row (k, t) of a rollout batch is index k * N + t everywhere (the
-// reference's xin layout, controller.py:272-275).
+// Rows are stored t-major on the device: row (k, t) is index t * K + k, so the
+// 32 lanes of a warp (consecutive rollouts) touch one contiguous span at every
+// step.  costs-to-go are kept t-major too and transposed to the reference's
+// (K, N) layout (controller.py:212) only when handed back through the API.
 #pragma once
 
 #include "common.cuh"
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kRolloutBlock)
   double ang[3] = {sa->state[6], sa->state[7], sa->state[8]};
   double rate[3] = {sa->state[9], sa->state[10], sa->state[11]};
   const double *ek = DEVICE_NOISE ? nullptr : eps + k * (int64_t)N * 4;
-  float4 *xk = xin + k * (int64_t)N;
+  float4 *xk = xin + k;  // row (k, t) at xk[t * K]
   constexpr int TB = 4;  // noise of TB steps is generated before their serial FP64 recurrence
   for (int t0 = 0; t0 < N; t0 += TB) {
     double e[TB][4];
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kRolloutBlock)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         u[c] = fmin(fmax(__dadd_rn(splan[4 * t + c], e[j][c]), dp.lo[c]), dp.hi[c]);
-      xk[t] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
+      xk[(int64_t)t * K] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
                           __double2float_rn(ang[2]), __double2float_rn(u[3]));
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   }
 
   for (int t = 0; t < N; ++t) {
-    const int64_t row = k * (int64_t)N + t;
+    const int64_t row = (int64_t)t * a.K + k;
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
     if (a.model == PI2_MODEL_HYBRID_LWPR) {
       const float4 m4 = a.lw_mean[row];
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       mn[0] = mn[1] = mn[2] = 0.0f;
       sd[2] = a.two_point;
     }
-    const float4 ap = (t + 1 < N) ? a.xin[row + 1] : a.ang_last[k];  // post-step attitude
+    const float4 ap = (t + 1 < N) ? a.xin[row + a.K] : a.ang_last[k];  // post-step attitude
     const float angterm = __fmul_rn(
         __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
     const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   // float64 suffix sum (controller.py:320-322) and ceiling (:243-246)
   const double dt = a.dp.dt, ceiling = sa->ceiling;
   double acc = 0.0;
-  double *out = a.costs + k * (int64_t)N;
+  double *out = a.costs + k;  // t-major: S(k, t) at out[t * K]
   for (int t = N - 1; t >= 0; --t) {
     const double s = __dmul_rn((double)sq[t * blockDim.x + threadIdx.x], dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       v = ceiling;
       crash = true;
     }
-    out[t] = v;
+    out[(int64_t)t * a.K] = v;
   }
   a.crash[k] = crash ? 1 : 0;
 }
@@ -655,20 +657,20 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n, apn = m4n;
   if (active) {
     if (hybrid) {
-      m4n = __ldg(a.lw_mean + kk * (int64_t)N);
-      s4n = __ldg(a.lw_std + kk * (int64_t)N);
+      m4n = __ldg(a.lw_mean + kk);
+      s4n = __ldg(a.lw_std + kk);
     }
-    apn = (1 < N) ? __ldg(a.xin + kk * (int64_t)N + 1) : __ldg(a.ang_last + kk);
+    apn = (1 < N) ? __ldg(a.xin + a.K + kk) : __ldg(a.ang_last + kk);
   }
   for (int t = 0; t < N; ++t) {
-    const int64_t row = kk * (int64_t)N + t;
+    const int64_t row = (int64_t)t * a.K + kk;
     const float4 m4 = m4n, s4 = s4n, ap = apn;
     if (active && t + 1 < N) {
       if (hybrid) {
-        m4n = __ldg(a.lw_mean + row + 1);
-        s4n = __ldg(a.lw_std + row + 1);
+        m4n = __ldg(a.lw_mean + row + a.K);
+        s4n = __ldg(a.lw_std + row + a.K);
       }
-      apn = (t + 2 < N) ? __ldg(a.xin + row + 2) : __ldg(a.ang_last + kk);
+      apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + kk);
     }
     float q = 0.0f;
     if (active) {
@@ -755,7 +757,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   if (!live || lane_g != 0) return;
   const double dt = a.dp.dt, ceiling = sa->ceiling;
   double acc = 0.0;
-  double *out = a.costs + k * (int64_t)N;
+  double *out = a.costs + k;  // t-major: S(k, t) at out[t * K]
   for (int t = N - 1; t >= 0; --t) {
     const double s = __dmul_rn((double)sq[t * RPB + grp], dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
@@ -764,7 +766,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       v = ceiling;
       crash = true;
     }
-    out[t] = v;
+    out[(int64_t)t * a.K] = v;
   }
   a.crash[k] = crash ? 1 : 0;
 }
@@ -787,9 +789,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __global__ void __launch_bounds__(32 * kChunkWarps)
-    partials_kernel(const double *__restrict__ costs, const double *__restrict__ eps,
-                    const StepArgs *__restrict__ sa, int iteration, int64_t K, int64_t k_off, int N,
-                    double neg_inv, double *__restrict__ out) {
+    partials_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
+                    const double *__restrict__ eps, const StepArgs *__restrict__ sa, int iteration,
+                    int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
   constexpr int J = kChunk / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.y * kChunkWarps + warp;  // one warp per (chunk, t)
@@ -800,7 +802,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int64_t k = k0 + lane + 32 * j;
-    s[j] = k < K ? __ldg(costs + k * N + t) : INFINITY;
+    s[j] = k < K ? __ldg(costs + k * cs_k + t * cs_t) : INFINITY;  // S(k, t)
     m = fmin(m, s[j]);
   }
   m = warp_min(m);
@@ -828,6 +830,25 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
   if (lane == 0) {
     double *o = out + ((int64_t)blockIdx.x * N + t) * PI2_PARTIAL_WIDTH;
     o[0] = m; o[1] = z; o[2] = v[0]; o[3] = v[1]; o[4] = v[2]; o[5] = v[3];
+  }
+}
+
+// t-major (N, K) -> reference (K, N), 32x32 tiles through shared memory
+__global__ void transpose_costs_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t K,
+                                       int N) {
+  __shared__ double tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  const int t0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int t = t0 + i;
+    const int64_t k = k0 + threadIdx.x;
+    if (t < N && k < K) tile[i][threadIdx.x] = src[(int64_t)t * K + k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i;
+    const int t = t0 + threadIdx.x;
+    if (t < N && k < K) dst[k * N + t] = tile[threadIdx.x][i];
   }
 }
 

@@ -361,7 +361,7 @@ int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool up
                      cudaStream_t st) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
   partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
-      ctx->d_costs, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+      ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
       ctx->d_partials);
   CU(cudaGetLastError());
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
@@ -591,7 +591,11 @@ int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan, c
   cudaStream_t st = pick(ctx, stream);
   TRY(stage_args(ctx, state, nullptr, ceiling, st));
   TRY(stage_plan(ctx, plan, st));
-  return launch_rollouts(ctx, 0, noise_dev, dyn_dev, costs_dev, crash_dev, st);
+  TRY(launch_rollouts(ctx, 0, noise_dev, dyn_dev, ctx->d_costs, crash_dev, st));
+  const dim3 tg((unsigned)((ctx->K + 31) / 32), (unsigned)((ctx->N + 31) / 32));
+  transpose_costs_kernel<<<tg, dim3(32, 8), 0, st>>>(ctx->d_costs, costs_dev, ctx->K, ctx->N);
+  CU(cudaGetLastError());
+  return PI2_OK;
 }
 
 int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise,
@@ -612,8 +616,10 @@ int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const do
     CU(cudaMemcpyAsync(ctx->d_dynbuf, dyn, sizeof(float) * K * M * N * 3, cudaMemcpyHostToDevice, st));
     dyn_dev = ctx->d_dynbuf;
   }
-  TRY(pi2_evaluate_device(ctx, state, plan, ctx->d_noise, dyn_dev, ceiling, ctx->d_costs, ctx->d_crash, st));
-  CU(cudaMemcpyAsync(costs_out, ctx->d_costs, sizeof(double) * K * N, cudaMemcpyDeviceToHost, st));
+  TRY(ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, sizeof(double) * K * N));
+  double *out = (double *)ctx->d_scratch;
+  TRY(pi2_evaluate_device(ctx, state, plan, ctx->d_noise, dyn_dev, ceiling, out, ctx->d_crash, st));
+  CU(cudaMemcpyAsync(costs_out, out, sizeof(double) * K * N, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(crash_out, ctx->d_crash, K, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return PI2_OK;
@@ -636,8 +642,8 @@ int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, co
   double *dplan = partials + PI2_PARTIAL_WIDTH * chunks * N;
   CU(cudaMemcpyAsync(dplan, plan, plbytes, cudaMemcpyHostToDevice, st));
   const double neg_inv = -1.0 / temperature;
-  partials_kernel<<<partials_grid(chunks, N), 32 * kChunkWarps, 0, st>>>(costs_dev, noise_dev, ctx->d_args, 0,
-                                                                         K, 0, N, neg_inv, partials);
+  partials_kernel<<<partials_grid(chunks, N), 32 * kChunkWarps, 0, st>>>(costs_dev, N, 1, noise_dev, ctx->d_args,
+                                                                         0, K, 0, N, neg_inv, partials);
   CU(cudaGetLastError());
   TRY(launch_combine(ctx, partials, chunks, N, neg_inv, nullptr, dplan, st));
   CU(cudaMemcpyAsync(plan_out, dplan, plbytes, cudaMemcpyDeviceToHost, st));
@@ -780,7 +786,7 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[3], st);
     partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
-        ctx->d_costs, nullptr, ctx->d_args, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+        ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
         ctx->d_partials);
     cudaEventRecord(ev[4], st);
     rc = launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, ctx->d_root, nullptr, st);
