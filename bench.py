@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=4096, help="rollouts in the CPU baseline sample")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--closed-loop-steps", type=int, default=200,
+                   help="control steps of the closed-loop trial (latency p50/p99); 0 disables")
     return p.parse_args()
 
 
@@ -374,6 +376,18 @@ def run_ours(args, rank: int, world: int, local: int):
         "clocks": clk,
         "gpu_launches": args.steps * (KERNELS_PER_ITER + (1 if world > 1 else 0)),
     }
+    if world == 1 and args.closed_loop_steps > 0:
+        gt = P.PerturbedModel(params, drag_coeff=0.08, thrust_scale=0.97)
+        trial = P.run_trial(task, P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=T, iterations_per_step=1),
+                            model, gt, seed=0, step_cap=args.closed_loop_steps, noise="device", device=local)
+        tl = np.sort(trial.step_latency_s) * 1e3
+        line["closed_loop"] = {
+            "what": "simworld.run_trial with device noise: latency of each receding_horizon_step (host state in, "
+                    "control out); plant = PerturbedModel(drag 0.08, thrust x0.97)",
+            "steps": int(trial.steps), "outcome": trial.outcome,
+            "p50_ms": float(np.median(tl)), "p99_ms": float(tl[min(len(tl) - 1, math.ceil(0.99 * len(tl)) - 1)]),
+            "max_ms": float(tl[-1]), "budget_ms": 20.0,
+        }
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(cfgd, args.cpu_sample, args.cpu_seconds)
         cb.pop("step_times_s", None)

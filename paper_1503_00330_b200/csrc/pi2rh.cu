@@ -505,6 +505,8 @@ int pi2_set_dynamics(pi2_ctx *ctx, const pi2_dynamics *d) {
   if (!ctx || !d) return fail(ctx, PI2_ERR_INVALID, "null argument");
   if (!(d->mass > 0) || !(d->dt > 0) || !(d->rate_gain > 0))
     return fail(ctx, PI2_ERR_INVALID, "mass, dt and rate_gain must be positive");
+  // DynParams are kernel arguments baked into the cached graph: re-capture only on change
+  if (ctx->have_dyn && std::memcmp(&ctx->dyn, d, sizeof(pi2_dynamics)) == 0) return PI2_OK;
   ctx->dyn = *d;
   DynParams &p = ctx->dp;
   p.dt = d->dt;
@@ -562,9 +564,9 @@ int pi2_select_model(pi2_ctx *ctx, int32_t kind, double param) {
     default:
       return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown model kind %d", kind);
   }
+  if (ctx->model != kind || ctx->model_param != param) invalidate_graph(ctx);
   ctx->model = kind;
   ctx->model_param = param;
-  invalidate_graph(ctx);
   return PI2_OK;
 }
 

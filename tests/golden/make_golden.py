@@ -241,9 +241,37 @@ def make_rng():
          angles=angles, wrapped=D.wrap_angle(angles))
 
 
+def make_trial():
+    """Closed loop: reference run_trial (simworld.py:270-380), plan with the control
+    model, advance a drag/thrust-biased PerturbedModel."""
+    p = D.QuadParams()
+    task = S.Task.default()
+    gt = D.PerturbedModel(p, drag_coeff=0.08, thrust_scale=0.97)
+    cases = {
+        "analytic": (D.AnalyticModel(p), C.PiConfig(num_rollouts=256, horizon_steps=30, iterations_per_step=1,
+                                                     temperature=0.5), 4, 60),
+        "hybrid": (ref_hybrid(synthetic.hybrid_stacks(24, seed=13)),
+                   C.PiConfig(num_rollouts=128, sub_rollouts=2, horizon_steps=20, iterations_per_step=2), 2, 40),
+    }
+    arrays = {}
+    for name, (model, cfg, seed, cap) in cases.items():
+        r = S.run_trial(task, cfg, model, gt, seed=seed, step_cap=cap)
+        arrays.update({f"{name}_rows": r.log_rows, f"{name}_outcome": np.array(r.outcome),
+                       f"{name}_steps": np.array(r.steps), f"{name}_total_cost": np.array(r.total_cost),
+                       f"{name}_avg_cost": np.array(r.avg_cost_per_sec_horizon),
+                       f"{name}_K": np.array(cfg.num_rollouts), f"{name}_M": np.array(cfg.sub_rollouts),
+                       f"{name}_N": np.array(cfg.horizon_steps), f"{name}_iters": np.array(cfg.iterations_per_step),
+                       f"{name}_temperature": np.array(cfg.temperature), f"{name}_seed": np.array(seed),
+                       f"{name}_cap": np.array(cap)})
+        print(name, r.outcome, r.steps, r.total_cost)
+    arrays.update(stack_arrays("hybrid_", synthetic.hybrid_stacks(24, seed=13)))
+    save("trial", **arrays)
+
+
 if __name__ == "__main__":
     make_rng()
     make_lwpr()
     make_eval()
     make_update()
     make_optimize()
+    make_trial()
