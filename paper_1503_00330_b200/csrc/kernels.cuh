@@ -159,7 +159,7 @@ struct LwprArgs {
   const float4 *x;      // (rows) inputs, padded to 4
   float *mean_out;      // [row * out_stride + axis - a_begin]
   float *sd_out;        // std (sqrt_out) or variance; may be null
-  int out_stride;
+  int out_stride;       // 4: float4 rows (xyz = axes, w = 0); 1: one axis
   int sqrt_out;
 };
 
@@ -422,6 +422,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
       const int64_t o = row * a.out_stride + (ax - a.a_begin);
       a.mean_out[o] = mean;
       if (VAR && a.sd_out) a.sd_out[o] = a.sqrt_out ? __fsqrt_rn(var) : var;
+      // float4 rows: the last pass also writes the pad lane, so every 32-byte
+      // sector is fully written while it sits in L2 (no read-for-ownership)
+      if (a.out_stride == 4 && ax == a.a_end - 1) {
+        a.mean_out[row * 4 + 3] = 0.0f;
+        if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
+      }
     }
   }
 }

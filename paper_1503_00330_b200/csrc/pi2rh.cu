@@ -151,7 +151,7 @@ int set_smem(pi2_ctx *ctx, F *fn, int bytes) {
 int lwpr_smem_limit(pi2_ctx *ctx) { return std::min(ctx->smem_optin, 64 * 1024); }
 
 template <int LAY, bool VAR, int R>
-int launch_lwpr_t(pi2_ctx *ctx, const LwprArgs &a, int smem, cudaStream_t st) {
+int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st) {
   auto *fn = lwpr_kernel<LAY, VAR, R>;
   TRY(set_smem(ctx, fn, smem));
   const int64_t per_block = (int64_t)kLwprBlock * R;
