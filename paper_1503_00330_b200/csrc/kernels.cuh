@@ -473,6 +473,7 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
   t = __fadd_rn(t, __fmul_rn(vz, vz));
   out = __fadd_rn(out, __fmul_rn(t, 0.1f));
   out = __fadd_rn(out, angterm);
+#pragma unroll 4
   for (int i = 0; i < c.n_obstacles; ++i) {
     float dx = __fsub_rn(px, c.obstacles[2 * i]);
     float dy = __fsub_rn(py, c.obstacles[2 * i + 1]);
@@ -483,7 +484,9 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
   return __fadd_rn(out, crashed ? 10.0f : 0.0f);
 }
 
-template <int MM>  // compile-time M (1..kMaxSmallM), or 0 = runtime M <= PI2_MAX_SUB_ROLLOUTS
+// MM: compile-time sub-rollouts held in registers (1), or 0 = runtime M <= PI2_MAX_SUB_ROLLOUTS.
+// FAST: hybrid LWPR model + navigation cost, branches folded at compile time.
+template <int MM, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   constexpr int MCAP = MM > 0 ? MM : PI2_MAX_SUB_ROLLOUTS;
   extern __shared__ float sq[];  // (N, blockDim): this thread's stage costs, column tid
@@ -502,7 +505,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
                        __double2float_rn(sa->state[5])};
   const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
   const uint64_t kg = (uint64_t)(a.k_off + k);
-  const bool threshold_cost = cost.kind == PI2_COST_THRESHOLD;
+  const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
+  const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
 
   float cs[MCAP][3], ccs[MCAP][3];
   bool crashed[MCAP];
@@ -516,14 +520,14 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
-    if (a.model == PI2_MODEL_HYBRID_LWPR) {
+    if (model == PI2_MODEL_HYBRID_LWPR) {
       const float4 m4 = a.lw_mean[row];
       mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
       if (a.spread) {
         const float4 s4 = a.lw_std[row];
         sd[0] = s4.x; sd[1] = s4.y; sd[2] = s4.z;
       }
-    } else if (a.model == PI2_MODEL_ANALYTIC) {  // dynamics.py:175-185
+    } else if (model == PI2_MODEL_ANALYTIC) {  // dynamics.py:175-185
       const float4 xr = a.xin[row];
       float sr, cr, sp, cp, sy, cy;
       sincosf(xr.x, &sr, &cr);
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
           const float *dp = a.dyn + ((k * M + m) * (int64_t)N + t) * 3;
           d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
         }
-        if (a.model == PI2_MODEL_TWO_POINT) {
+        if (model == PI2_MODEL_TWO_POINT) {
           d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
         }
 #pragma unroll
@@ -631,7 +635,9 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
 // butterfly reproduces it exactly (adjacent pairs at every level, IEEE add
 // is commutative); otherwise lane 0 replays the reference loop from shared
 // memory.  Lane 0 of the group owns the float64 suffix sum.
-template <int G>
+// FAST: hybrid LWPR model, device dynamics noise, navigation cost (the
+// real-time configuration) with every branch folded at compile time.
+template <int G, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a) {
   constexpr int RPB = kRolloutBlock / G;  // rollouts per block
   extern __shared__ float sq[];           // (N, RPB) stage costs
@@ -653,12 +659,15 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
                        __double2float_rn(sa->state[5])};
   const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
   const uint64_t kg = (uint64_t)(a.k_off + k);
-  const bool threshold_cost = cost.kind == PI2_COST_THRESHOLD;
+  const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const int64_t kk = live ? k : 0;
+  const bool device_dyn = FAST || a.device_dyn;
+  const bool two_point = !FAST && a.model == PI2_MODEL_TWO_POINT;
+  const uint64_t dyn_base = (kg * (uint64_t)S + (uint64_t)m) * (uint64_t)N;  // counter of (k, m, t=0)
 
   float cs[3] = {-0.0f, -0.0f, -0.0f}, ccs[3] = {-0.0f, -0.0f, -0.0f};
   bool crashed = false;
-  const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
+  const bool hybrid = FAST || a.model == PI2_MODEL_HYBRID_LWPR;
   // rows of step t+1 are loaded while step t computes (hides HBM latency)
   float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n, apn = m4n;
   if (active) {
@@ -692,14 +701,14 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
           __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
       const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
       float d[3];
-      if (a.device_dyn) {
-        const float4 z = normals4((kg * (uint64_t)S + (uint64_t)m) * (uint64_t)N + (uint64_t)t, dk0, dk1);
+      if (device_dyn) {
+        const float4 z = normals4(dyn_base + (uint64_t)t, dk0, dk1);
         d[0] = z.x; d[1] = z.y; d[2] = z.z;
       } else {
         const float *dp = a.dyn + ((kk * S + m) * (int64_t)N + t) * 3;
         d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
       }
-      if (a.model == PI2_MODEL_TWO_POINT) {
+      if (two_point) {
         d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
       }
       float pos[3], vel[3];

@@ -215,9 +215,9 @@ bool spread(const pi2_ctx *ctx) {
   return prob && ctx->M > 1;
 }
 
-template <int MM>
+template <int MM, bool FAST>
 int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
-  auto *fn = rollout_kernel<MM>;
+  auto *fn = rollout_kernel<MM, FAST>;
   const int smem = a.N * kRolloutBlock * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + kRolloutBlock - 1) / kRolloutBlock;
@@ -226,9 +226,9 @@ int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   return PI2_OK;
 }
 
-template <int G>
+template <int G, bool FAST>
 int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
-  auto *fn = rollout_group_kernel<G>;
+  auto *fn = rollout_group_kernel<G, FAST>;
   constexpr int RPB = kRolloutBlock / G;
   const int smem = a.N * RPB * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
@@ -238,17 +238,26 @@ int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   return PI2_OK;
 }
 
+template <int G>
+int launch_group_g(pi2_ctx *ctx, const RollArgs &a, bool fast, cudaStream_t st) {
+  return fast ? launch_group_t<G, true>(ctx, a, st) : launch_group_t<G, false>(ctx, a, st);
+}
+
 int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int S = a.spread ? a.M : 1;
+  const bool nav = ctx->cost.kind == PI2_COST_NAVIGATION;
+  const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
   // sub-rollouts on lanes (any model but the analytic one, which is never spread)
   if (S > 1 && S <= 32) {
-    if (S <= 2) return launch_group_t<2>(ctx, a, st);
-    if (S <= 4) return launch_group_t<4>(ctx, a, st);
-    if (S <= 8) return launch_group_t<8>(ctx, a, st);
-    if (S <= 16) return launch_group_t<16>(ctx, a, st);
-    return launch_group_t<32>(ctx, a, st);
+    const bool fast = hybrid && nav && a.device_dyn;
+    if (S <= 2) return launch_group_g<2>(ctx, a, fast, st);
+    if (S <= 4) return launch_group_g<4>(ctx, a, fast, st);
+    if (S <= 8) return launch_group_g<8>(ctx, a, fast, st);
+    if (S <= 16) return launch_group_g<16>(ctx, a, fast, st);
+    return launch_group_g<32>(ctx, a, fast, st);
   }
-  return S == 1 ? launch_rollout_t<1>(ctx, a, st) : launch_rollout_t<0>(ctx, a, st);
+  if (S == 1) return (hybrid && nav) ? launch_rollout_t<1, true>(ctx, a, st) : launch_rollout_t<1, false>(ctx, a, st);
+  return launch_rollout_t<0, false>(ctx, a, st);
 }
 
 int check_ready(pi2_ctx *ctx) {
@@ -576,6 +585,7 @@ int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *c) {
     return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown cost kind %d", c->kind);
   if (c->n_obstacles < 0 || c->n_obstacles > PI2_MAX_OBSTACLES)
     return fail(ctx, PI2_ERR_UNSUPPORTED, "at most %d obstacles", PI2_MAX_OBSTACLES);
+  if (ctx->have_cost && ctx->cost.kind != c->kind) invalidate_graph(ctx);  // kernel variant depends on it
   ctx->cost = *c;
   ctx->have_cost = true;
   return PI2_OK;
