@@ -70,6 +70,7 @@ struct DynParams {
 struct AxisHeader {
   float g0, gs[4];  // global linear shift g(x) = g0 + gs.x folded out of the local models
   float qd[10];     // shared metric: log2e * (-1/2 x'Dx) coefficients (Q00 Q01 Q02 Q03 Q11 Q12 Q13 Q22 Q23 Q33)
+  float mu[4];      // shared metric: inputs are centred, x~ = x - mu (mean field centre); 0 otherwise
   int num_fields;
   int64_t offset;   // float offset of the axis' first record
 };

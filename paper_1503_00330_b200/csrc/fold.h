@@ -57,6 +57,14 @@ inline void fold_axis(const AxisRaw &a, int layout, std::vector<float> &rec, Axi
   const int RS = record_floats(layout);
   const size_t base = rec.size();
   rec.resize(base + (size_t)a.L * RS, 0.0f);
+  // shared metric: centre inputs on the mean field centre so the per-row
+  // quadratic q(x~) stays small (the kernels may then drop it, see lwpr_kernel)
+  double mu[4] = {0, 0, 0, 0};
+  if (layout == kLayShared) {
+    for (int l = 0; l < a.L; ++l)
+      for (int i = 0; i < a.d; ++i) mu[i] += a.centers[(size_t)l * a.d + i];
+    for (double &v : mu) v /= a.L;
+  }
   std::vector<double> y0(a.L), s(4 * (size_t)a.L, 0.0);
   double g0 = 0.0, gs[4] = {0, 0, 0, 0};
   for (int l = 0; l < a.L; ++l) {
@@ -64,7 +72,7 @@ inline void fold_axis(const AxisRaw &a, int layout, std::vector<float> &rec, Axi
     for (int i = 0; i < a.d; ++i) {
       const double si = a.coefs[(size_t)l * (a.d + 1) + 1 + i];
       s[4 * (size_t)l + i] = si;
-      yy -= si * a.centers[(size_t)l * a.d + i];  // y0 = coef0 - s.c (lwpr.py:355-357)
+      yy -= si * (a.centers[(size_t)l * a.d + i] - mu[i]);  // y0 = coef0 - s.c (lwpr.py:355-357), in x~
     }
     y0[l] = yy;
     g0 += yy;
@@ -74,7 +82,10 @@ inline void fold_axis(const AxisRaw &a, int layout, std::vector<float> &rec, Axi
   for (double &v : gs) v /= a.L;
   h = AxisHeader{};
   h.g0 = (float)g0;
-  for (int i = 0; i < 4; ++i) h.gs[i] = (float)gs[i];
+  for (int i = 0; i < 4; ++i) {
+    h.gs[i] = (float)gs[i];
+    h.mu[i] = (float)mu[i];
+  }
   h.num_fields = a.L;
   h.offset = (int64_t)base;
   double D0[4][4] = {{0}};
@@ -89,7 +100,7 @@ inline void fold_axis(const AxisRaw &a, int layout, std::vector<float> &rec, Axi
   for (int l = 0; l < a.L; ++l) {
     double c[4] = {0, 0, 0, 0}, D[4][4] = {{0}};
     for (int i = 0; i < a.d; ++i) {
-      c[i] = a.centers[(size_t)l * a.d + i];
+      c[i] = a.centers[(size_t)l * a.d + i] - mu[i];
       for (int j = 0; j < a.d; ++j) D[i][j] = a.metrics[((size_t)l * a.d + i) * a.d + j];
     }
     double dc[4], a0 = 0.0;
@@ -122,8 +133,7 @@ inline void fold_axis(const AxisRaw &a, int layout, std::vector<float> &rec, Axi
       f[19] = (float)(y0[l] - g0);
       f[20] = (float)a.lvar[l];
     } else {
-      // the 2^64 shift lives in the per-row quadratic (shared_qrow)
-      f[0] = (float)(a0 * kLog2e);
+      f[0] = (float)(a0 * kLog2e + kExpShift);
       for (int i = 0; i < 4; ++i) {
         f[1 + i] = (float)(dc[i] * kLog2e);
         f[5 + i] = (float)(s[4 * (size_t)l + i] - gs[i]);

@@ -224,7 +224,7 @@ __device__ __forceinline__ float field_lvar(const float *f) {
   return f[Lay<LAY>::LV];
 }
 
-// per-row log2-scaled quadratic of a shared metric, plus the 2^64 shift
+// per-row log2-scaled quadratic of a shared metric at centred x~
 __device__ __forceinline__ float shared_qrow(const AxisHeader &h, const float4 &x) {
   float r = fmaf(h.qd[0], x.x, fmaf(h.qd[1], x.y, fmaf(h.qd[2], x.z, h.qd[3] * x.w)));
   float q = r * x.x;
@@ -232,9 +232,14 @@ __device__ __forceinline__ float shared_qrow(const AxisHeader &h, const float4 &
   q = fmaf(r, x.y, q);
   r = fmaf(h.qd[7], x.z, h.qd[8] * x.w);
   q = fmaf(r, x.z, q);
-  q = fmaf(h.qd[9] * x.w, x.w, q);
-  return __fadd_rn(q, (float)kExpShift);
+  return fmaf(h.qd[9] * x.w, x.w, q);
 }
+
+// Rows whose centred quadratic q~ >= this (log2 units) take the field loop
+// WITHOUT the per-field "+ q~" add: every accumulator is linear in the weight,
+// so a per-row factor 2^-q~ cancels in mean and variance, and 2^(logit2 - q~)
+// stays below 2^(64 + 60) (no overflow).  The decision is warp-uniform.
+constexpr float kNearQ = -60.0f;
 
 // Reference-exact evaluation of one row (rare: every weight is (nearly)
 // denormal in float32).  Emulates numpy: e = expf(q) with float32 denormal
@@ -279,7 +284,7 @@ __device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, 
 // dispatch without starving the FMA pipe (profiles/micro/mufu_mix.cu).
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-template <int LAY>
+template <int LAY, bool ADDQ>
 __device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *X, float2 Q) {
   if (LAY == kLayDiag) {
     float2 lg = __ffma2_rn(__ffma2_rn(bc(f[1]), X[0], bc(f[5])), X[0], bc(f[0]));
@@ -306,7 +311,7 @@ __device__ __forceinline__ float2 field_logit2_x2(const float *f, const float2 *
     lg = __ffma2_rn(bc(f[2]), X[1], lg);
     lg = __ffma2_rn(bc(f[3]), X[2], lg);
     lg = __ffma2_rn(bc(f[4]), X[3], lg);
-    return __fadd2_rn(lg, Q);
+    return ADDQ ? __fadd2_rn(lg, Q) : lg;
   }
 }
 
@@ -317,6 +322,37 @@ __device__ __forceinline__ float2 field_local_x2(const float *f, const float2 *X
   y = __ffma2_rn(bc(f[S + 1]), X[1], y);
   y = __ffma2_rn(bc(f[S + 2]), X[2], y);
   return __ffma2_rn(bc(f[S + 3]), X[3], y);
+}
+
+// The field loop of one tile: P row pairs, accumulators updated in place.
+template <int LAY, bool VAR, int P, bool ADDQ>
+__device__ __forceinline__ void lwpr_fields(const float *sp, int nl, const float2 (*X)[4], const float2 *Q, float2 *den,
+                                            float2 *num, float2 *m2, float2 *lv) {
+  constexpr int RS = Lay<LAY>::RS;
+#pragma unroll 2
+  for (int l = 0; l < nl; ++l) {
+    float f[RS];
+#pragma unroll
+    for (int i = 0; i < RS / 4; ++i) {
+      const float4 v = reinterpret_cast<const float4 *>(sp + (int64_t)l * RS)[i];
+      f[4 * i + 0] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float2 lg = field_logit2_x2<LAY, ADDQ>(f, X[p], Q[p]);
+      const float2 e = make_float2(ex2_ftz(lg.x), ex2_ftz(lg.y));
+      const float2 y = field_local_x2<LAY>(f, X[p]);
+      den[p] = __fadd2_rn(den[p], e);
+      if (VAR) {
+        const float2 ey = __fmul2_rn(e, y);
+        num[p] = __fadd2_rn(num[p], ey);
+        m2[p] = __ffma2_rn(ey, y, m2[p]);
+        lv[p] = __ffma2_rn(e, bc(field_lvar<LAY>(f)), lv[p]);
+      } else {
+        num[p] = __ffma2_rn(e, y, num[p]);
+      }
+    }
+  }
 }
 
 template <int LAY, bool VAR, int R, int BLOCK = kLwprBlock, int MINB = 4>
@@ -354,12 +390,26 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
   for (int ax = a.a_begin; ax < a.a_end; ++ax) {
     const AxisHeader h = a.axis[ax];
     float2 den[P], num[P], m2[P], lv[P], Q[P];
+    float2 XT[P][4];  // centred inputs x~ = x - mu
+    float4 xt[R];
+    bool near_mine = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      xt[r] = make_float4(__fsub_rn(x[r].x, h.mu[0]), __fsub_rn(x[r].y, h.mu[1]), __fsub_rn(x[r].z, h.mu[2]),
+                          __fsub_rn(x[r].w, h.mu[3]));
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       den[p] = num[p] = m2[p] = lv[p] = make_float2(0.0f, 0.0f);
-      Q[p] = LAY == kLayShared ? make_float2(shared_qrow(h, x[2 * p]), shared_qrow(h, x[2 * p + 1]))
+      Q[p] = LAY == kLayShared ? make_float2(shared_qrow(h, xt[2 * p]), shared_qrow(h, xt[2 * p + 1]))
                                : make_float2(0.0f, 0.0f);
+      near_mine = near_mine && Q[p].x >= kNearQ && Q[p].y >= kNearQ;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float *v0 = reinterpret_cast<const float *>(&xt[2 * p]), *v1 = reinterpret_cast<const float *>(&xt[2 * p + 1]);
+        XT[p][i] = make_float2(v0[i], v1[i]);
+      }
     }
+    const bool near = __all_sync(0xffffffffu, near_mine);
 
     const int tile = a.resident ? h.num_fields : a.tile;
     for (int l0 = 0; l0 < h.num_fields; l0 += tile) {
@@ -374,30 +424,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
         __syncthreads();
         sp = srec;
       }
-#pragma unroll 2
-      for (int l = 0; l < nl; ++l) {
-        float f[RS];
-#pragma unroll
-        for (int i = 0; i < RS / 4; ++i) {
-          const float4 v = reinterpret_cast<const float4 *>(sp + (int64_t)l * RS)[i];
-          f[4 * i + 0] = v.x; f[4 * i + 1] = v.y; f[4 * i + 2] = v.z; f[4 * i + 3] = v.w;
-        }
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const float2 lg = field_logit2_x2<LAY>(f, X[p], Q[p]);
-          const float2 e = make_float2(ex2_ftz(lg.x), ex2_ftz(lg.y));
-          const float2 y = field_local_x2<LAY>(f, X[p]);
-          den[p] = __fadd2_rn(den[p], e);
-          if (VAR) {
-            const float2 ey = __fmul2_rn(e, y);
-            num[p] = __fadd2_rn(num[p], ey);
-            m2[p] = __ffma2_rn(ey, y, m2[p]);
-            lv[p] = __ffma2_rn(e, bc(field_lvar<LAY>(f)), lv[p]);
-          } else {
-            num[p] = __ffma2_rn(e, y, num[p]);
-          }
-        }
-      }
+      if (LAY == kLayShared && near)
+        lwpr_fields<LAY, VAR, P, false>(sp, nl, XT, Q, den, num, m2, lv);
+      else
+        lwpr_fields<LAY, VAR, P, LAY == kLayShared>(sp, nl, XT, Q, den, num, m2, lv);
     }
 
 #pragma unroll
@@ -410,14 +440,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
       const float sm2 = (r & 1) ? m2[p].y : m2[p].x;
       const float slv = (r & 1) ? lv[p].y : lv[p].x;
       const float qr = (r & 1) ? Q[p].y : Q[p].x;
-      const float gx = fmaf(h.gs[3], x[r].w, fmaf(h.gs[2], x[r].z, fmaf(h.gs[1], x[r].y, fmaf(h.gs[0], x[r].x, h.g0))));
+      const float gx = fmaf(h.gs[3], xt[r].w, fmaf(h.gs[2], xt[r].z, fmaf(h.gs[1], xt[r].y, fmaf(h.gs[0], xt[r].x, h.g0))));
+      // normaliser on the 2^(logit*log2e + 64) scale (the fast loop dropped 2^q~)
+      const float dn_scaled = (LAY == kLayShared && near) ? dn * exp2f(qr) : dn;
       float mean, var = 0.0f;
-      if (dn >= kSlowDen) {
+      if (dn_scaled >= kSlowDen) {
         const float mp = __fdiv_rn(nm, dn);
         mean = __fadd_rn(gx, mp);
         if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(sm2, slv), dn), __fmul_rn(mp, mp)), 0.0f);
       } else {
-        lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, x[r], qr, gx, &mean, &var);
+        lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, xt[r], qr, gx, &mean, &var);
       }
       const int64_t o = row * a.out_stride + (ax - a.a_begin);
       a.mean_out[o] = mean;
