@@ -241,6 +241,26 @@ def make_rng():
          angles=angles, wrapped=D.wrap_angle(angles))
 
 
+def make_persistence():
+    """An LWPR1 payload written by the reference's save_model (lwpr.py:261-285) from a
+    model trained with the reference's RLS update (so its fields share d_init)."""
+    m = LW.LwprModel(input_dim=4, d_init=[30.0, 30.0, 30.0, 1500.0], ridge=1e-4)
+    r = np.random.default_rng(31)
+    for _ in range(400):
+        x = r.uniform([-0.35, -0.35, -0.35, 0.1], [0.35, 0.35, 0.35, 0.28])
+        m.update(x, float(np.sin(x[0]) * x[3] / 0.019 + 0.01 * r.normal()))
+    blob = LW.save_model(m)
+    X = r.uniform([-0.4, -0.4, -0.4, 0.05], [0.4, 0.4, 0.4, 0.33], size=(200, 4)).astype(np.float32)
+    fr = LW.FrozenLwpr(m, batch_rows=200)
+    mean = np.empty(200, np.float32)
+    var = np.empty(200, np.float32)
+    fr.predict_into(X, mean, var)
+    c, mt, cf, lv = m._stacks()
+    save("persistence", blob=np.frombuffer(blob, np.uint8), X=X, mean=mean, var=var, centers=c, metrics=mt,
+         coefs=cf, lvar=lv, num_fields=np.array(m.num_fields))
+    print("persistence: fields", m.num_fields)
+
+
 def make_trial():
     """Closed loop: reference run_trial (simworld.py:270-380), plan with the control
     model, advance a drag/thrust-biased PerturbedModel."""
@@ -275,3 +295,4 @@ if __name__ == "__main__":
     make_update()
     make_optimize()
     make_trial()
+    make_persistence()

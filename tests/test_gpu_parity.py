@@ -371,3 +371,41 @@ def test_sharded_partials_are_gpu_count_invariant():
             out = np.empty((cfg.horizon_steps, 4))
             c.call("pi2_read_plan", _abi.ptr(out), None)
             np.testing.assert_array_equal(out, single.controls)
+
+
+@pytest.mark.parametrize("L,full", [(1500, False), (700, True)])
+def test_tiled_parameters_match_oracle(L, full):
+    """Parameter sets too large for shared memory stream through in tiles (C3's path)."""
+    stacks = synthetic.hybrid_stacks(L, seed=L, full_metric=full)
+    if not full:  # per-field metrics -> the diagonal layout, 16 floats/field: 3*1500*64 B > 64 KB
+        stacks = tuple(synthetic.AxisStack(s.centers, s.metrics * (1.0 + 1e-3 * np.arange(L))[:, None, None],
+                                           s.coefs, s.lvar) for s in stacks)
+    K, N, M = 96, 12, 2
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=3)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn)
+    plan = P.ControlPlan.hover(params, N)
+    noise = P.sample_noise(cfg, 0, 0)
+    dyn = P.sample_dynamics_noise(cfg, 0, 0)
+    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn)
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise,
+                         RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES), dyn, M)
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
+def test_shared_metric_model_from_reference_training():
+    """A model trained by the reference (fields share d_init) through the LWPR1 format."""
+    z = load("persistence")
+    m = P.load_model(z["blob"].tobytes())
+    fr = P.FrozenLwpr(m, len(z["X"]))
+    mean = np.empty(len(z["X"]), np.float32)
+    var = np.empty(len(z["X"]), np.float32)
+    fr.predict_into(z["X"], mean, var)
+    scale = max(1.0, float(np.abs(z["mean"]).max()))
+    np.testing.assert_allclose(mean, z["mean"], atol=2e-5 * scale)
+    np.testing.assert_allclose(var, z["var"], rtol=1e-3, atol=2e-5 * scale)
