@@ -18,6 +18,7 @@ constexpr int kChunk = 256;         // rollouts per leaf partial (fixed => G-inv
 constexpr int kChunkWarps = 8;      // warps per partials block
 constexpr int kSeg = 1024;          // leaves per combine segment
 constexpr int kMaxSmallM = 8;       // sub-rollouts held in registers
+constexpr int64_t kWideMaxK = 16384; // up to this K, attitude/rollout use a warp per rollout (latency)
 constexpr double kPi = 3.141592653589793;        // np.pi
 constexpr double kTwoPi = 6.283185307179586;     // 2.0 * math.pi
 constexpr double kLog2e = 1.4426950408889634;

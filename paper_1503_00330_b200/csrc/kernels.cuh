@@ -819,6 +819,159 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
 }
 
 // ---------------------------------------------------------------------------
+// Small-K (latency) variants: one warp per rollout.  Work that is independent
+// across timesteps (noise, clipping, stage costs) is spread over the lanes;
+// only the true recurrences stay serial, each on its own lane: the FP64
+// attitude/rate recurrence per channel (lanes 0-2), the FP32 cumsum per
+// component (lanes 0-2) and the FP64 suffix sum (lane 0).  Same arithmetic,
+// same order as the thread-per-rollout kernels -> identical results.
+// ---------------------------------------------------------------------------
+constexpr int kWideWarps = 4;  // rollouts per block
+
+template <bool DEVICE_NOISE>
+__global__ void __launch_bounds__(32 * kWideWarps)
+    attitude_wide_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
+                         const double *__restrict__ eps, int iteration, int64_t K, int64_t k_off, int N,
+                         DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last) {
+  extern __shared__ double wsm[];
+  double *splan = wsm;                                   // (N, 4)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *u = splan + 4 * N + (size_t)warp * 4 * N;      // (N, 4) clipped controls of this rollout
+  float4 *stage = reinterpret_cast<float4 *>(splan + 4 * N + (size_t)kWideWarps * 4 * N) + (size_t)warp * (N + 1);
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) splan[i] = plan[i];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * kWideWarps + warp;
+  if (k >= K) return;
+  for (int t = lane; t < N; t += 32) {
+    double e[4];
+    if (DEVICE_NOISE) {
+      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
+      e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[4 * t + c] = fmin(fmax(__dadd_rn(splan[4 * t + c], e[c]), dp.lo[c]), dp.hi[c]);
+    reinterpret_cast<float *>(&stage[t])[3] = __double2float_rn(u[4 * t + 3]);
+  }
+  __syncwarp();
+  if (lane < 3) {
+    const int c = lane;
+    double ang = sa->state[6 + c], rate = sa->state[9 + c];
+    for (int t = 0; t < N; ++t) {
+      reinterpret_cast<float *>(&stage[t])[c] = __double2float_rn(ang);
+      ang = wrap_angle(__dadd_rn(ang, __dmul_rn(rate, dp.dt)));
+      rate = __dadd_rn(rate, __dmul_rn(dp.gain_dt, __dsub_rn(u[4 * t + c], rate)));
+    }
+    reinterpret_cast<float *>(&stage[N])[c] = __double2float_rn(ang);
+  }
+  __syncwarp();
+  for (int t = lane; t < N; t += 32) xin[(int64_t)t * K + k] = stage[t];
+  if (lane == 0) ang_last[k] = make_float4(stage[N].x, stage[N].y, stage[N].z, 0.0f);
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs a) {
+  extern __shared__ float fsm[];
+  __shared__ pi2_cost cost;
+  if (threadIdx.x == 0) cost = a.sa->cost;
+  __syncthreads();
+  const int N = a.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per warp: acc (N,3) -> cs (N,3), ccs (N,3), angterm (N), q (N)
+  float *acc = fsm + (size_t)warp * 9 * N, *cs = acc + 3 * N, *ccs = cs + 3 * N;
+  float *angt = fsm + (size_t)kWideWarps * 9 * N + (size_t)warp * 2 * N, *q = angt + N;
+  const int64_t k = (int64_t)blockIdx.x * kWideWarps + warp;
+  if (k >= a.K) return;
+  const StepArgs *sa = a.sa;
+  const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
+  const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
+  for (int t = lane; t < N; t += 32) {
+    const int64_t row = (int64_t)t * a.K + k;
+    float mn[3];
+    if (model == PI2_MODEL_HYBRID_LWPR) {
+      const float4 m4 = __ldg(a.lw_mean + row);
+      mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
+    } else if (model == PI2_MODEL_ANALYTIC) {
+      const float4 xr = __ldg(a.xin + row);
+      float sr, cr, sp, cp, sy, cy;
+      sincosf(xr.x, &sr, &cr);
+      sincosf(xr.y, &sp, &cp);
+      sincosf(xr.z, &sy, &cy);
+      const float fm = __fmul_rn(xr.w, a.dp.inv_m32);
+      const float crsp = __fmul_rn(cr, sp);
+      mn[0] = __fmul_rn(fm, __fadd_rn(__fmul_rn(crsp, cy), __fmul_rn(sr, sy)));
+      mn[1] = __fmul_rn(fm, __fsub_rn(__fmul_rn(crsp, sy), __fmul_rn(sr, cy)));
+      mn[2] = __fsub_rn(__fmul_rn(fm, __fmul_rn(cr, cp)), a.dp.g32);
+    } else {
+      mn[0] = mn[1] = mn[2] = 0.0f;
+    }
+    acc[3 * t] = mn[0]; acc[3 * t + 1] = mn[1]; acc[3 * t + 2] = mn[2];
+    const float4 ap = (t + 1 < N) ? __ldg(a.xin + row + a.K) : __ldg(a.ang_last + k);
+    angt[t] = __fmul_rn(__fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)),
+                        0.2f);
+  }
+  __syncwarp();
+  if (lane < 3) {  // np.cumsum twice, sequential (controller.py:294-295)
+    float s = -0.0f, ss = -0.0f;
+    for (int t = 0; t < N; ++t) {
+      s = __fadd_rn(s, acc[3 * t + lane]);
+      ss = __fadd_rn(ss, s);
+      cs[3 * t + lane] = s;
+      ccs[3 * t + lane] = ss;
+    }
+  }
+  __syncwarp();
+  const float p0[3] = {__double2float_rn(sa->state[0]), __double2float_rn(sa->state[1]),
+                       __double2float_rn(sa->state[2])};
+  const float v0[3] = {__double2float_rn(sa->state[3]), __double2float_rn(sa->state[4]),
+                       __double2float_rn(sa->state[5])};
+  bool carry = false;  // persistent crash indicator up to the previous 32 steps
+  for (int t0 = 0; t0 < N; t0 += 32) {
+    const int t = t0 + lane;
+    float pos[3] = {0, 0, 0}, vel[3] = {0, 0, 0};
+    bool now = false;
+    if (t < N) {
+      const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        vel[c] = __fadd_rn(__fmul_rn(cs[3 * t + c], a.dp.dt32), v0[c]);
+        pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[3 * t + c], cs[3 * t + c]), a.dp.dt2_32),
+                                     __fmul_rn(sdt, v0[c])), p0[c]);
+      }
+      now = !threshold_cost && ((pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
+                                (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) ||
+                                (pos[1] > cost.arena_hi[1]) || (pos[2] > cost.arena_hi[2]));
+    }
+    // logical_or.accumulate along t (controller.py:306): prefix OR via ballot
+    const unsigned b = __ballot_sync(0xffffffffu, now);
+    const bool crashed = carry || (b & (0xffffffffu >> (31 - lane))) != 0;
+    carry = carry || b != 0;
+    if (t < N)
+      q[t] = threshold_cost ? (pos[2] > cost.threshold ? 1.0f : 0.0f)
+                            : nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  bool crash = carry;
+  const double dt = a.dp.dt, ceiling = sa->ceiling;
+  double s = 0.0;
+  double *out = a.costs + k;
+  for (int t = N - 1; t >= 0; --t) {
+    const double v = __dmul_rn((double)q[t], dt);
+    s = (t == N - 1) ? v : __dadd_rn(s, v);
+    double w = s;
+    if (!isfinite(w)) {
+      w = ceiling;
+      crash = true;
+    }
+    out[(int64_t)t * a.K] = w;
+  }
+  a.crash[k] = crash ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
 // K11a: leaf partials of the per-timestep softmax (controller.py:367-370):
 // per chunk of kChunk rollouts and per t: m = min S, Z = sum w, V = sum w eps,
 // w = exp((S - m) * neg_inv).  Warp w handles t = w, w + 8, ...; lane order and

@@ -256,6 +256,19 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     if (S <= 16) return launch_group_g<16>(ctx, a, fast, st);
     return launch_group_g<32>(ctx, a, fast, st);
   }
+  if (S == 1 && a.K <= kWideMaxK) {  // latency regime: a warp per rollout
+    const unsigned grid = (unsigned)((a.K + kWideWarps - 1) / kWideWarps);
+    const int smem = kWideWarps * 11 * a.N * (int)sizeof(float);
+    if (hybrid && nav) {
+      TRY(set_smem(ctx, rollout_wide_kernel<true>, smem));
+      rollout_wide_kernel<true><<<grid, 32 * kWideWarps, smem, st>>>(a);
+    } else {
+      TRY(set_smem(ctx, rollout_wide_kernel<false>, smem));
+      rollout_wide_kernel<false><<<grid, 32 * kWideWarps, smem, st>>>(a);
+    }
+    CU(cudaGetLastError());
+    return PI2_OK;
+  }
   if (S == 1) return (hybrid && nav) ? launch_rollout_t<1, true>(ctx, a, st) : launch_rollout_t<1, false>(ctx, a, st);
   return launch_rollout_t<0, false>(ctx, a, st);
 }
@@ -305,7 +318,21 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   const int N = ctx->N;
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
   const int psmem = 4 * N * (int)sizeof(double);
-  if (noise_dev) {
+  if (K <= kWideMaxK) {  // latency regime: a warp per rollout
+    const unsigned wgrid = (unsigned)((K + kWideWarps - 1) / kWideWarps);
+    const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
+    if (noise_dev) {
+      TRY(set_smem(ctx, attitude_wide_kernel<false>, wsmem));
+      attitude_wide_kernel<false><<<wgrid, 32 * kWideWarps, wsmem, st>>>(
+          ctx->d_args, ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
+          ctx->d_ang_last);
+    } else {
+      TRY(set_smem(ctx, attitude_wide_kernel<true>, wsmem));
+      attitude_wide_kernel<true><<<wgrid, 32 * kWideWarps, wsmem, st>>>(
+          ctx->d_args, ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
+          ctx->d_ang_last);
+    }
+  } else if (noise_dev) {
     TRY(set_smem(ctx, attitude_kernel<false>, psmem));
     attitude_kernel<false><<<grid, kRolloutBlock, psmem, st>>>(
         ctx->d_args, ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp,

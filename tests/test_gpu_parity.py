@@ -70,9 +70,13 @@ def test_evaluate_matches_reference_golden(name):
     assert np.all(du_err(new.controls, z["new_plan"], z["plan"]) < DU_TOL)
 
 
+# K <= 16384 runs the warp-per-rollout (latency) kernels, larger K the
+# thread-per-rollout / lane-per-sub-rollout ones: both are covered.
 @pytest.mark.parametrize("K,N,L,M,full", [(2048, 50, 100, 4, False), (1500, 50, 100, 1, False),
                                           (777, 20, 40, 3, True), (300, 10, 20, 16, False),
-                                          (1, 1, 5, 1, False), (129, 7, 9, 8, False)])
+                                          (1, 1, 5, 1, False), (129, 7, 9, 8, False), (33, 70, 12, 1, False),
+                                          (20000, 30, 24, 1, False), (20000, 24, 24, 4, False),
+                                          (17000, 20, 16, 3, True)])
 def test_evaluate_matches_oracle(K, N, L, M, full):
     stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
     params = P.QuadParams()
