@@ -34,14 +34,23 @@ def shard_range(num_rollouts: int, rank: int, world: int, chunk: int | None = No
 
 
 def gather_partials(partial, group=None):
-    """All-gather a (N, 6) partial from every rank into (G, N, 6), rank order."""
+    """All-gather a (N, 6) partial from every rank into (G, N, 6), rank order.
+
+    NCCL gathers the device tensor in place on the current stream; a gloo
+    group (CPU tests, several ranks sharing one GPU) stages through the host.
+    """
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    out = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
-    dist.all_gather_into_tensor(out, partial.contiguous(), group=group)
-    return out
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
+        dist.all_gather_into_tensor(out, partial.contiguous(), group=group)
+        return out
+    host = partial.detach().to("cpu")  # synchronises with the kernels that wrote it
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.stack(parts).to(partial.device)
 
 
 def combine_gathered_host(gathered: np.ndarray, temperature: float) -> np.ndarray:
