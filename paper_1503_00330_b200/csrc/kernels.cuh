@@ -491,6 +491,23 @@ __device__ __forceinline__ float sign_of(float v) {  // np.sign (0 -> 0, NaN -> 
   return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : v);
 }
 
+// The cost plugin stays in shared memory (holding it in registers cost
+// occupancy in the lane-per-sub-rollout kernel).
+// crash_now: floor contact or arena exit (simworld.py:157-164)
+__device__ __forceinline__ bool nav_crash_now(const pi2_cost &c, float px, float py, float pz) {
+  return (pz <= c.z_floor) || (px < c.arena_lo[0]) || (px > c.arena_hi[0]) || (py < c.arena_lo[1]) ||
+         (py > c.arena_hi[1]) || (pz > c.arena_hi[2]);
+}
+
+// obstacle term 100 exp(-10 d^2): __expf = ex2.approx(x log2e); its error is
+// <= 2e-7 of the stage cost it contributes to (the term bounds the cost).
+__device__ __forceinline__ float obstacle_term(float px, float py, float ox, float oy) {
+  const float dx = __fsub_rn(px, ox), dy = __fsub_rn(py, oy);
+  const float t = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+  return __fmul_rn(__expf(__fmul_rn(t, -10.0f)), 100.0f);
+}
+
+// stage cost q(x) in the reference's float32 operation order (simworld.py:166-198)
 __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, float py, float pz,
                                                 float vx, float vy, float vz, float angterm,
                                                 bool crashed) {
@@ -505,14 +522,11 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
   t = __fadd_rn(t, __fmul_rn(vz, vz));
   out = __fadd_rn(out, __fmul_rn(t, 0.1f));
   out = __fadd_rn(out, angterm);
-#pragma unroll 4
-  for (int i = 0; i < c.n_obstacles; ++i) {
-    float dx = __fsub_rn(px, c.obstacles[2 * i]);
-    float dy = __fsub_rn(py, c.obstacles[2 * i + 1]);
-    t = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-    t = __fmul_rn(expf(__fmul_rn(t, -10.0f)), 100.0f);
-    out = __fadd_rn(out, t);
-  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < c.n_obstacles) out = __fadd_rn(out, obstacle_term(px, py, c.obstacles[2 * i], c.obstacles[2 * i + 1]));
+  for (int i = 4; i < c.n_obstacles; ++i)
+    out = __fadd_rn(out, obstacle_term(px, py, c.obstacles[2 * i], c.obstacles[2 * i + 1]));
   return __fadd_rn(out, crashed ? 10.0f : 0.0f);
 }
 
@@ -539,6 +553,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   const uint64_t kg = (uint64_t)(a.k_off + k);
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
+  const pi2_cost &nav = cost;
 
   float cs[MCAP][3], ccs[MCAP][3];
   bool crashed[MCAP];
@@ -613,10 +628,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       if (threshold_cost) {
         q[m] = pos[2] > cost.threshold ? 1.0f : 0.0f;
       } else {
-        crashed[m] = crashed[m] || (pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
-                     (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) ||
-                     (pos[1] > cost.arena_hi[1]) || (pos[2] > cost.arena_hi[2]);
-        q[m] = nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[m]);
+        crashed[m] = crashed[m] || nav_crash_now(nav, pos[0], pos[1], pos[2]);
+        q[m] = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[m]);
       }
     }
     // sub-rollout mean: pairwise halving while even, plain mean when odd
@@ -692,6 +705,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
   const uint64_t kg = (uint64_t)(a.k_off + k);
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
+  const pi2_cost &nav = cost;
   const int64_t kk = live ? k : 0;
   const bool device_dyn = FAST || a.device_dyn;
   const bool two_point = !FAST && a.model == PI2_MODEL_TWO_POINT;
@@ -756,10 +770,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       if (threshold_cost) {
         q = pos[2] > cost.threshold ? 1.0f : 0.0f;
       } else {
-        crashed = crashed || (pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
-                  (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) || (pos[1] > cost.arena_hi[1]) ||
-                  (pos[2] > cost.arena_hi[2]);
-        q = nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed);
+        crashed = crashed || nav_crash_now(nav, pos[0], pos[1], pos[2]);
+        q = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed);
       }
     }
     float qm;
@@ -887,6 +899,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
   const StepArgs *sa = a.sa;
   const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
+  const pi2_cost &nav = cost;
   for (int t = lane; t < N; t += 32) {
     const int64_t row = (int64_t)t * a.K + k;
     float mn[3];
@@ -940,9 +953,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
         pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[3 * t + c], cs[3 * t + c]), a.dp.dt2_32),
                                      __fmul_rn(sdt, v0[c])), p0[c]);
       }
-      now = !threshold_cost && ((pos[2] <= cost.z_floor) || (pos[0] < cost.arena_lo[0]) ||
-                                (pos[0] > cost.arena_hi[0]) || (pos[1] < cost.arena_lo[1]) ||
-                                (pos[1] > cost.arena_hi[1]) || (pos[2] > cost.arena_hi[2]));
+      now = !threshold_cost && nav_crash_now(nav, pos[0], pos[1], pos[2]);
     }
     // logical_or.accumulate along t (controller.py:306): prefix OR via ballot
     const unsigned b = __ballot_sync(0xffffffffu, now);
@@ -950,7 +961,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
     carry = carry || b != 0;
     if (t < N)
       q[t] = threshold_cost ? (pos[2] > cost.threshold ? 1.0f : 0.0f)
-                            : nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
+                            : nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
   }
   __syncwarp();
   if (lane != 0) return;
