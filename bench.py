@@ -215,11 +215,18 @@ def run_ours(args, rank: int, world: int, local: int):
     from paper_1503_00330_b200.simworld import cost_struct
 
     dist = None
+    # one rank per GPU; PI2_DIST_BACKEND=gloo lets several ranks share a GPU to
+    # exercise the multi-rank path where only one GPU exists (timings meaningless)
+    backend = os.environ.get("PI2_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     cfgd, desc = workload(args.config)
     K, T, L, M = cfgd["K"], cfgd["T"], cfgd["L"], cfgd["M"]
@@ -267,7 +274,7 @@ def run_ours(args, rank: int, world: int, local: int):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -370,7 +377,7 @@ def run_ours(args, rank: int, world: int, local: int):
             "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
             "flops_per_launch": lwpr_flops,
             "flops_per_field": flops_per_field,
-            "traffic": lwpr_traffic(args.config),
+            "traffic": lwpr_traffic(args.config) if world == 1 else None,
         },
         "stages_ms": stages,
         "clocks": clk,
