@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 
 #include "fold.h"
 #include "kernels.cuh"
+#include "lwpr_tc.cuh"
 
 using namespace pi2;
 
@@ -44,6 +46,13 @@ struct pi2_ctx {
   AxisHeader hdr[3]{};
   float *d_params = nullptr;
   size_t params_cap = 0;
+  // tensor-core LWPR operands (shared-metric models, lwpr_tc.cuh)
+  bool tc_ok = false;
+  bool tc_enabled = true;  // PI2_LWPR_TC=0 forces the CUDA-core kernel
+  LwprTcArgs tc{};
+  float *d_tc = nullptr;
+  size_t tc_cap = 0;
+  int tc_smem = 0;
 
   // device workspaces (sized by dims)
   StepArgs *d_args = nullptr;
@@ -137,6 +146,26 @@ int ensure_params(pi2_ctx *ctx) {
     CU(cudaMemcpy(ctx->d_params, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
   ctx->layout = layout;
+  // tensor-core operands when every axis shares its metric and has 4 inputs
+  ctx->tc_ok = false;
+  if (ctx->tc_enabled && ctx->axes[0].L > 0 && ctx->axes[1].L > 0 && ctx->axes[2].L > 0) {
+    std::vector<float> blob;
+    LwprTcArgs ta{};
+    if (build_tc_weights(ctx->axes, blob, ta)) {
+      TRY(ensure(ctx, (void **)&ctx->d_tc, &ctx->tc_cap, blob.size() * sizeof(float)));
+      CU(cudaMemcpy(ctx->d_tc, blob.data(), blob.size() * sizeof(float), cudaMemcpyHostToDevice));
+      ta.w = ctx->d_tc;
+      int64_t wmax = 0;
+      for (int i = 0; i < 3; ++i) {
+        const int64_t we = i < 2 ? ta.axis_off[i + 1] : ta.w_floats;
+        wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
+      }
+      // padded so that exactly kTcCtasPerSm CTAs (and their TMEM) fit on an SM
+      ctx->tc_smem = std::max((int)((wmax * 4 + 127) / 128 * 128 + 8192), 228 * 1024 / kTcCtasPerSm - 2048);
+      ctx->tc = ta;
+      ctx->tc_ok = ctx->tc_smem <= ctx->smem_optin;
+    }
+  }
   ctx->params_dirty = false;
   return PI2_OK;
 }
@@ -161,9 +190,35 @@ int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st) {
   return PI2_OK;
 }
 
+template <bool VAR>
+int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out, float *sd_out, cudaStream_t st) {
+  LwprTcArgs a = ctx->tc;
+  for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
+  a.params = ctx->d_params;
+  a.rows = rows;
+  a.x = x;
+  a.mean_out = mean_out;
+  a.sd_out = sd_out;
+  a.sqrt_out = 1;
+  auto *fn = lwpr_tc_kernel<VAR>;
+  TRY(set_smem(ctx, fn, ctx->tc_smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int64_t tiles = (rows + 127) / 128;
+  const int64_t grid = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles) * 3;  // CTA i -> axis i % 3
+  fn<<<(unsigned)grid, kTcThreads, ctx->tc_smem, st>>>(a);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
 int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
                 float *sd_out, int stride, int sqrt_out, cudaStream_t st) {
   TRY(ensure_params(ctx));
+  // all three axes with variance into float4 rows (the sub-rollout path): tensor
+  // cores when eligible.  Measured on B200 (profiles/README.md): 491 vs 510 us at
+  // C2; the mean-only CUDA-core loop (10 FMA-pipe ops/field) stays faster.
+  if (ctx->tc_ok && sd_out && a_begin == 0 && a_end == 3 && stride == 4 && sqrt_out)
+    return launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st);
   LwprArgs a{};
   a.params = ctx->d_params;
   for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
@@ -484,6 +539,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   };
   if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (const char *e = getenv("PI2_LWPR_TC")) ctx->tc_enabled = std::atoi(e) != 0;
   const int64_t K = ctx->K, N = ctx->N;
   ctx->n_chunks = (K + kChunk - 1) / kChunk;
 #define ALLOC(p, bytes)                                                               \
@@ -524,7 +580,7 @@ void pi2_destroy(pi2_ctx *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   invalidate_graph(ctx);
-  void *bufs[] = {ctx->d_params, ctx->d_args,   ctx->d_plan,  ctx->d_plan2,    ctx->d_xin,
+  void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_args,   ctx->d_plan,  ctx->d_plan2,    ctx->d_xin,
                   ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
                   ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch};
   for (void *p : bufs)
