@@ -197,11 +197,11 @@ def measured_peaks():
         return {}
 
 
-def lwpr_traffic(config: str):
+def lwpr_traffic(config: str, tc: bool):
     """dram bytes per LWPR launch from a committed `ncu --set full` capture, if any."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "lwpr_traffic.json")))
-        return d.get(config)
+        return d.get(config + ("_tc" if tc else ""))
     except (OSError, ValueError):
         return None
 
@@ -334,6 +334,10 @@ def run_ours(args, rank: int, world: int, local: int):
     flops_per_field = 32 if M > 1 else 27  # 27 (+5 variance) per (row, axis, field)
     lwpr_flops = rows * 3 * L * flops_per_field
     achieved = lwpr_flops / (stages["lwpr"] / 1e3) / 1e12
+    # which LWPR kernel ran: the tcgen05 one for the variance path unless disabled
+    tc = M > 1 and os.environ.get("PI2_LWPR_TC", "1") != "0"
+    exps = rows * 3 * L  # one MUFU ex2 per (row, axis, field)
+    mufu_peak = float(peaks.get("mufu_ex2_per_s", 4.60e12))
     clk = clocks.summary()
     peak_obs = n_sm * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12 if clk.get("sm_mhz") else None
     h2d = 12 * 8 + T * 4 * 8 + 8 * (12 + 4 * 16 + 4 + 2) + 4 * 48  # state + plan + StepArgs
@@ -368,7 +372,8 @@ def run_ours(args, rank: int, world: int, local: int):
         "latency_ms": {"p50": p50, "p99": p99, "what": "e2e control step (host state/plan -> control)"},
         "roofline": {
             "bound": "fp32",
-            "kernel": "lwpr_kernel",
+            "kernel": "lwpr_tc_kernel (tcgen05 3xTF32 field GEMM + CUDA-core exp/moments)" if tc
+                      else "lwpr_kernel (CUDA cores, FFMA2)",
             "achieved": achieved,
             "peak": peak_tflops,
             "unit": "TFLOP/s",
@@ -377,7 +382,10 @@ def run_ours(args, rank: int, world: int, local: int):
             "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
             "flops_per_launch": lwpr_flops,
             "flops_per_field": flops_per_field,
-            "traffic": lwpr_traffic(args.config) if world == 1 else None,
+            "traffic": lwpr_traffic(args.config, tc) if world == 1 else None,
+            "mufu": {"ex2_per_launch": exps, "achieved_per_s": exps / (stages["lwpr"] / 1e3),
+                     "peak_per_s": mufu_peak, "frac": exps / (stages["lwpr"] / 1e3) / mufu_peak,
+                     "peak_source": "profiles/micro/mufu_mix_b200.txt (MUFU-only ex2 stream)"},
         },
         "stages_ms": stages,
         "clocks": clk,

@@ -16,8 +16,14 @@
 // 32w..32w+31 = tile rows; thread 0 issues the 3 MMAs and commits to an
 // mbarrier; operands are K-major, no swizzle (8x16B core matrices,
 // LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups).
-// Persistent CTAs keep all axes' W in shared memory; 2 CTAs per SM (256 TMEM
-// columns each) overlap one CTA's MMA with the other's exp phase.
+// CTAs are axis-specialised (CTA i handles axis i % 3, tiles i / 3, i / 3 +
+// gridDim / 3, ...) so only one axis' W sits in shared memory; 4 CTAs per SM
+// (128 TMEM columns each, shared-memory request padded so no 5th CTA spins in
+// tcgen05.alloc) overlap one CTA's MMA + TMEM latency with the others' exp
+// phase.  Used for the variance path only: with 4 moments per field the
+// CUDA-core kernel issues 14 FMA-pipe ops per field pair and the GEMM offload
+// wins (C2 491 vs 510 us); the mean-only loop (10 ops) is already faster than
+// this kernel's per-chunk synchronisation.
 #pragma once
 
 #include <vector>
@@ -103,9 +109,90 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
                  "=r"((r)[6]), "=r"((r)[7])                                                            \
                : "r"(addr))
 
-constexpr int kTcThreads = 128;  // 4 warps: warp w owns TMEM lanes 32w..32w+31 (tile rows)
-constexpr int kTcCtasPerSm = PI2_TC_CTAS;  // co-resident CTAs: their MMA phases interleave
+#define PI2_TMEM_WAIT16(a, b)                                                                      \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                   \
+               : "+r"((a)[0]), "+r"((a)[1]), "+r"((a)[2]), "+r"((a)[3]), "+r"((a)[4]), "+r"((a)[5]),  \
+                 "+r"((a)[6]), "+r"((a)[7]), "+r"((b)[0]), "+r"((b)[1]), "+r"((b)[2]), "+r"((b)[3]),  \
+                 "+r"((b)[4]), "+r"((b)[5]), "+r"((b)[6]), "+r"((b)[7])                               \
+               :                                                                                   \
+               : "memory")
 
+constexpr int kTcThreads = 128;  // warp w owns TMEM lanes 32w .. 32w + 31 (tile rows)
+constexpr int kTcCtasPerSm = PI2_TC_CTAS;  // co-resident CTAs: their MMA phases interleave
+constexpr int kTcABytes = 8192;  // one A operand: hi | lo, 128 rows x 8 tf32 each
+
+#ifdef PI2_TC_PROF
+__device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barrier, MMA wait, exp, tail
+#define PI2_TC_T(i)                          \
+  {                                          \
+    const long long t_ = clock64();          \
+    prof[i] += t_ - t_last;                  \
+    t_last = t_;                             \
+  }
+#else
+#define PI2_TC_T(i)
+#endif
+
+// 8 fields of one row: e = 2^logit, moments on field pairs
+template <bool VAR>
+__device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *yy, const float *slv, float2 &den,
+                                           float2 &num, float2 &m2, float2 &lv) {
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) {
+    const float2 e = make_float2(ex2_ftz(__uint_as_float(lg[i])), ex2_ftz(__uint_as_float(lg[i + 1])));
+    const float2 y = make_float2(__uint_as_float(yy[i]), __uint_as_float(yy[i + 1]));
+    den = __fadd2_rn(den, e);
+    if (VAR) {
+      const float2 ey = __fmul2_rn(e, y);
+      num = __fadd2_rn(num, ey);
+      m2 = __ffma2_rn(ey, y, m2);
+      lv = __ffma2_rn(e, *reinterpret_cast<const float2 *>(slv + i), lv);
+    } else {
+      num = __ffma2_rn(e, y, num);
+    }
+  }
+}
+
+// centred inputs and q~ of one row; its features [x~, 1, q~, 0, 0] as tf32 hi and lo
+// into the A operand (K-major, no swizzle)
+__device__ __forceinline__ void tc_features(const AxisHeader &h, float4 x, uint8_t *sa, int r, float4 &xt, float &q) {
+  xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]), __fsub_rn(x.w, h.mu[3]));
+  q = shared_qrow(h, xt);
+  const float f[8] = {xt.x, xt.y, xt.z, xt.w, 1.0f, q, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float hi = tf32_rna(f[k]);
+    *reinterpret_cast<float *>(sa + umma_kmajor_off(r, k)) = hi;
+    *reinterpret_cast<float *>(sa + 4096 + umma_kmajor_off(r, k)) = tf32_rna(__fsub_rn(f[k], hi));
+  }
+}
+
+// mean / std of one row from its moments (exact path when the normaliser underflowed)
+template <bool VAR>
+__device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeader &h, int ax, int64_t row, float4 xt,
+                                            float q, float dn, float nm, float m2, float lv) {
+  if (row >= a.rows) return;
+  const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
+  float mean, var = 0.0f;
+  if (dn >= kSlowDen) {
+    const float mp = __fdiv_rn(nm, dn);
+    mean = __fadd_rn(gx, mp);
+    if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(m2, lv), dn), __fmul_rn(mp, mp)), 0.0f);
+  } else {
+    lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
+  }
+  a.mean_out[row * 4 + ax] = mean;
+  if (VAR && a.sd_out) a.sd_out[row * 4 + ax] = a.sqrt_out ? __fsqrt_rn(var) : var;
+  if (ax == 2) {
+    a.mean_out[row * 4 + 3] = 0.0f;
+    if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
+  }
+}
+
+// Per CTA the tiles are software-pipelined: while the tensor core computes the
+// first chunk of tile t, the CUDA cores finalize tile t - 1 and write tile t + 1's
+// features into the other A buffer (its x was loaded one tile ahead), so only the
+// barrier, the MMA latency and the exp phase remain on the critical path.
 template <bool VAR>
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprTcArgs a) {
   extern __shared__ __align__(128) uint8_t tsm[];
@@ -118,7 +205,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   const int64_t nlv = (int64_t)a.nchunks[ax] * kTcChunk;
   float *sw = reinterpret_cast<float *>(tsm);
   float *slv_base = sw + (wend - wbeg);
-  uint8_t *sa = tsm + (((wend - wbeg + nlv) * 4 + 127) / 128) * 128;  // A_hi | A_lo, 4 KB each
+  uint8_t *sa = tsm + (((wend - wbeg + nlv) * 4 + 127) / 128) * 128;  // two A operands
   const int tid = threadIdx.x, warp = tid >> 5;
 
   for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
@@ -135,111 +222,105 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_addr));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
+  const AxisHeader &h = a.axis[ax];
+  const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
+  const int64_t tstride = gridDim.x / 3;
+  int64_t tile = blockIdx.x / 3;
+  float4 xt, xt_prev = make_float4(0.f, 0.f, 0.f, 0.f);
+  float q, q_prev = 0.0f, dn_p = 0.0f, nm_p = 0.0f, m2_p = 0.0f, lv_p = 0.0f;
+  int64_t row_prev = a.rows;  // nothing to finalize yet
+  {
+    const int64_t r0 = tile * 128 + tid;
+    tc_features(h, __ldg(a.x + (r0 < last ? r0 : last)), sa, tid, xt, q);
+  }
+  int64_t rn = (tile + tstride) * 128 + tid;
+  float4 xn = __ldg(a.x + (rn < last ? rn : last));  // next tile's inputs, one tile ahead
+
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
   const uint32_t tmem_lane = tmem + ((uint32_t)(warp * 32) << 16);
-  const uint32_t sa_addr = (uint32_t)__cvta_generic_to_shared(sa);
   const uint32_t sw_addr = (uint32_t)__cvta_generic_to_shared(sw);
   uint32_t phase = 0;
+  int buf = 0;
+#ifdef PI2_TC_PROF
+  long long prof[5] = {0, 0, 0, 0, 0}, t_last = clock64();
+#endif
 
-  const int64_t ntiles = (a.rows + 127) / 128;
-  const int64_t tstride = gridDim.x / 3;
-  for (int64_t tile = blockIdx.x / 3; tile < ntiles; tile += tstride) {
-    const int64_t row = tile * 128 + tid;
-    const float4 x = __ldg(a.x + (row < a.rows ? row : a.rows - 1));
-    {
-      const AxisHeader h = a.axis[ax];
-      const float4 xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]),
-                                    __fsub_rn(x.w, h.mu[3]));
-      const float q = shared_qrow(h, xt);
-      {  // row features, hi and lo tf32 parts, into the A operands
-        const float f[8] = {xt.x, xt.y, xt.z, xt.w, 1.0f, q, 0.0f, 0.0f};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float hi = tf32_rna(f[k]);
-          *reinterpret_cast<float *>(sa + umma_kmajor_off(tid, k)) = hi;
-          *reinterpret_cast<float *>(sa + 4096 + umma_kmajor_off(tid, k)) = tf32_rna(__fsub_rn(f[k], hi));
-        }
-      }
-      float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;
-      int64_t woff = 0;  // within this axis' block in shared memory
-      for (int c = 0; c < a.nchunks[ax]; ++c) {
-        const int lc = a.chunk_pad[ax][c];  // fields of this chunk, multiple of 8, 2 lc <= 128 columns
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();  // A written, TMEM free
-        if (tid == 0) {
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
-          const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
-          const uint32_t wb = sw_addr + (uint32_t)(woff * 4);
-          const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
-          mma_tf32(tmem, a_hi, b_hi, idesc, 0);
-          mma_tf32(tmem, a_hi, b_lo, idesc, 1);
-          mma_tf32(tmem, a_lo, b_hi, idesc, 1);
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              mbar_addr));
-        }
-        mbar_wait(mbar_addr, phase);
-        phase ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const float *slv = slv_base + (int64_t)c * kTcChunk;
-        for (int j = 0; j < lc; j += 16) {
-          const int nb = min(2, (lc - j) >> 3);
-          uint32_t lg[16], yy[16];
-          PI2_TMEM_LD8(lg, tmem_lane + j);
-          PI2_TMEM_LD8(yy, tmem_lane + lc + j);
-          if (nb == 2) {
-            PI2_TMEM_LD8(lg + 8, tmem_lane + j + 8);
-            PI2_TMEM_LD8(yy + 8, tmem_lane + lc + j + 8);
-          }
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            if (i >= 8 * nb) break;
-            const float2 e = make_float2(ex2_ftz(__uint_as_float(lg[i])), ex2_ftz(__uint_as_float(lg[i + 1])));
-            const float2 y = make_float2(__uint_as_float(yy[i]), __uint_as_float(yy[i + 1]));
-            den = __fadd2_rn(den, e);
-            if (VAR) {
-              const float2 ey = __fmul2_rn(e, y);
-              num = __fadd2_rn(num, ey);
-              m2 = __ffma2_rn(ey, y, m2);
-              lv = __ffma2_rn(e, *reinterpret_cast<const float2 *>(slv + j + i), lv);
-            } else {
-              num = __ffma2_rn(e, y, num);
-            }
-          }
-        }
-        woff += (int64_t)2 * (2 * lc * 8);
-      }
+  for (; tile < ntiles; tile += tstride, buf ^= 1) {
+    const uint32_t sa_addr = (uint32_t)__cvta_generic_to_shared(sa + buf * kTcABytes);
+    float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;
+    float4 xt_next = xt;
+    float q_next = q;
+    int64_t woff = 0;  // within this axis' block in shared memory
+    for (int c = 0; c < a.nchunks[ax]; ++c) {
+      const int lc = a.chunk_pad[ax][c];  // fields of this chunk, multiple of 8, 2 lc <= 128 columns
+      asm volatile("fence.proxy.async.shared::cta;");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      if (row < a.rows) {
-        const float dn = __fadd_rn(den.x, den.y), nm = __fadd_rn(num.x, num.y);
-        const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
-        float mean, var = 0.0f;
-        if (dn >= kSlowDen) {
-          const float mp = __fdiv_rn(nm, dn);
-          mean = __fadd_rn(gx, mp);
-          if (VAR) {
-            const float s2 = __fadd_rn(__fadd_rn(m2.x, m2.y), __fadd_rn(lv.x, lv.y));
-            var = fmaxf(__fsub_rn(__fdiv_rn(s2, dn), __fmul_rn(mp, mp)), 0.0f);
-          }
-        } else {
-          lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
-        }
-        a.mean_out[row * 4 + ax] = mean;
-        if (VAR && a.sd_out) a.sd_out[row * 4 + ax] = a.sqrt_out ? __fsqrt_rn(var) : var;
-        if (ax == 2) {
-          a.mean_out[row * 4 + 3] = 0.0f;
-          if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
-        }
+      __syncthreads();  // A written, TMEM free
+      PI2_TC_T(1);
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
+        const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
+        const uint32_t wb = sw_addr + (uint32_t)(woff * 4);
+        const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
+        mma_tf32(tmem, a_hi, b_hi, idesc, 0);
+        mma_tf32(tmem, a_hi, b_lo, idesc, 1);
+        mma_tf32(tmem, a_lo, b_hi, idesc, 1);
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            mbar_addr));
       }
+      if (c == 0) {  // in the MMA's shadow: finish tile t - 1, stage tile t + 1
+        tc_finalize<VAR>(a, h, ax, row_prev, xt_prev, q_prev, dn_p, nm_p, m2_p, lv_p);
+        if (tile + tstride < ntiles) {
+          tc_features(h, xn, sa + (buf ^ 1) * kTcABytes, tid, xt_next, q_next);
+          rn = (tile + 2 * tstride) * 128 + tid;
+          xn = __ldg(a.x + (rn < last ? rn : last));
+        }
+        PI2_TC_T(0);
+      }
+      mbar_wait(mbar_addr, phase);
+      phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      PI2_TC_T(2);
+      const float *slv = slv_base + (int64_t)c * kTcChunk;
+      const int nb = lc >> 3;  // 8-field batches, two per TMEM wait
+      for (int b = 0; b < nb; b += 2) {
+        uint32_t la[8], ya[8], lb[8], yb[8];
+        PI2_TMEM_LD8(la, tmem_lane + 8 * b);
+        PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b);
+        if (b + 1 < nb) {
+          PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
+          PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+        }
+        PI2_TMEM_WAIT16(la, ya);
+        PI2_TMEM_WAIT16(lb, yb);
+        tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
+        if (b + 1 < nb) tc_fields8<VAR>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+      }
+      woff += (int64_t)2 * (2 * lc * 8);
+      PI2_TC_T(3);
     }
+    xt_prev = xt;
+    q_prev = q;
+    row_prev = tile * 128 + tid;
+    dn_p = __fadd_rn(den.x, den.y);
+    nm_p = __fadd_rn(num.x, num.y);
+    m2_p = __fadd_rn(m2.x, m2.y);
+    lv_p = __fadd_rn(lv.x, lv.y);
+    xt = xt_next;
+    q = q_next;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
+  tc_finalize<VAR>(a, h, ax, row_prev, xt_prev, q_prev, dn_p, nm_p, m2_p, lv_p);
+  PI2_TC_T(4);
+#ifdef PI2_TC_PROF
+  if ((tid & 31) == 0)
+    for (int i = 0; i < 5; ++i) atomicAdd(&g_tc_prof[i], (unsigned long long)prof[i]);
+#endif
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols));
@@ -255,6 +336,17 @@ inline float host_tf32_rna(float v) {
   float r;
   std::memcpy(&r, &b, 4);
   return r;
+}
+
+// Dynamic shared memory of lwpr_tc_kernel: this axis' W + variances + the two A
+// operands, padded so that exactly kTcCtasPerSm CTAs (and so their TMEM
+// allocations) fit on an SM (228 KB per SM, 1 KB reserved per CTA).
+inline int tc_smem_bytes(int64_t w_axis_floats, const void *fn) {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  const int need = (int)((w_axis_floats * 4 + 127) / 128 * 128 + 2 * kTcABytes);
+  const int cap = 228 * 1024 / kTcCtasPerSm - 1024 - (int)fa.sharedSizeBytes - 256;
+  return need > cap ? -1 : cap;  // -1: this axis' weights do not fit at full residency
 }
 
 inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, LwprTcArgs &ta) {

@@ -160,10 +160,9 @@ int ensure_params(pi2_ctx *ctx) {
         const int64_t we = i < 2 ? ta.axis_off[i + 1] : ta.w_floats;
         wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
       }
-      // padded so that exactly kTcCtasPerSm CTAs (and their TMEM) fit on an SM
-      ctx->tc_smem = std::max((int)((wmax * 4 + 127) / 128 * 128 + 8192), 228 * 1024 / kTcCtasPerSm - 2048);
+      ctx->tc_smem = tc_smem_bytes(wmax, (const void *)lwpr_tc_kernel<true>);
       ctx->tc = ta;
-      ctx->tc_ok = ctx->tc_smem <= ctx->smem_optin;
+      ctx->tc_ok = ctx->tc_smem > 0 && ctx->tc_smem <= ctx->smem_optin;
     }
   }
   ctx->params_dirty = false;

@@ -68,11 +68,12 @@ int main(int argc, char **argv) {
     wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
   }
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
-  const int smem2 = std::max((int)((wmax * 4 + 127) / 128 * 128 + 8192), 228 * 1024 / kTcCtasPerSm - 2048);
   auto *k2 = lwpr_tc_kernel<true>;
+  const int smem2 = tc_smem_bytes(wmax, (const void *)k2);
   cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned g2 = (kTcCtasPerSm * sms) / 3 * 3;
+  printf("CTAS %d CHUNK %d\n", PI2_TC_CTAS, PI2_TC_CHUNK);
   printf("rows %lld L %d: W %lld floats, lv %lld, smem tc %d B, chunks %d pad %d\n", (long long)rows, L,
          (long long)ta.w_floats, (long long)ta.lv_floats, smem2, ta.nchunks[0], ta.chunk_pad[0][0]);
 
@@ -87,6 +88,17 @@ int main(int argc, char **argv) {
   cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
   cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k2<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
   cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+#ifdef PI2_TC_PROF
+  {
+    unsigned long long pr[5];
+    cudaMemcpyFromSymbol(pr, g_tc_prof, sizeof(pr));
+    double tot = 0;
+    for (auto v : pr) tot += (double)v;
+    const double n = 6.0 * ((rows + 127) / 128) * 3 * kTcThreads / 32;  // warp-tile-axes over 6 launches
+    printf("clocks per warp-tile-axis: features+finalize %.0f  barrier %.0f  mma-wait %.0f  exp %.0f  tail %.0f  total %.0f\n",
+           pr[0] / n, pr[1] / n, pr[2] / n, pr[3] / n, pr[4] / n, tot / n);
+  }
+#endif
   std::vector<float> a1(rows * 4), b1(rows * 4), a2(rows * 4), b2(rows * 4);
   cudaMemcpy(a1.data(), m1, rows * 16, cudaMemcpyDeviceToHost); cudaMemcpy(b1.data(), s1, rows * 16, cudaMemcpyDeviceToHost);
   cudaMemcpy(a2.data(), m2, rows * 16, cudaMemcpyDeviceToHost); cudaMemcpy(b2.data(), s2, rows * 16, cudaMemcpyDeviceToHost);
@@ -103,5 +115,25 @@ int main(int argc, char **argv) {
          flops / (ms1 / 5) / 1e9, ms2 / 5 * 1e3, flops / (ms2 / 5) / 1e9);
   printf("max |dmean| %.3e (max |mean| %.2f), max rel dstd %.3e, nan/inf %lld\n", dm, mm, ds, (long long)bad);
   printf("sample: cc %f %f tc %f %f\n", a1[0], b1[0], a2[0], b2[0]);
+  {  // mean only (M = 1 rollouts)
+    auto *k3 = lwpr_kernel<kLayShared, false, 8>;
+    cudaFuncSetAttribute((const void *)k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+    auto *k4 = lwpr_tc_kernel<false>;
+    cudaFuncSetAttribute((const void *)k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    la.sd_out = nullptr;
+    ta.sd_out = nullptr;
+    k3<<<g1, 128, smem1>>>(la);
+    k4<<<g2, kTcThreads, smem2>>>(ta);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k3<<<g1, 128, smem1>>>(la); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k4<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+    cudaMemcpy(a1.data(), m1, rows * 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(a2.data(), m2, rows * 16, cudaMemcpyDeviceToHost);
+    double dm0 = 0;
+    for (int64_t i = 0; i < rows * 4; ++i) dm0 = fmax(dm0, fabs(a1[i] - a2[i]));
+    printf("mean-only  cuda-core: %8.1f us   tensor-core: %8.1f us   max |dmean| %.3e   (%s)\n", ms1 / 5 * 1e3,
+           ms2 / 5 * 1e3, dm0, cudaGetErrorString(cudaDeviceSynchronize()));
+  }
   return 0;
 }
