@@ -70,6 +70,7 @@ int main(int argc, char **argv) {
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
   auto *k2 = lwpr_tc_kernel<true>;
   const int smem2 = tc_smem_bytes(wmax, (const void *)k2);
+  if (smem2 < 0) { printf("W does not fit %d CTAs/SM\n", kTcCtasPerSm); return 1; }
   cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned g2 = (kTcCtasPerSm * sms) / 3 * 3;
@@ -94,7 +95,7 @@ int main(int argc, char **argv) {
     cudaMemcpyFromSymbol(pr, g_tc_prof, sizeof(pr));
     double tot = 0;
     for (auto v : pr) tot += (double)v;
-    const double n = 6.0 * ((rows + 127) / 128) * 3 * kTcThreads / 32;  // warp-tile-axes over 6 launches
+    const double n = 6.0 * ((rows + 127) / 128) * 3 * 4;  // warp-tile-axes over 6 launches (4 row warps per CTA)
     printf("clocks per warp-tile-axis: features+finalize %.0f  barrier %.0f  mma-wait %.0f  exp %.0f  tail %.0f  total %.0f\n",
            pr[0] / n, pr[1] / n, pr[2] / n, pr[3] / n, pr[4] / n, tot / n);
   }
