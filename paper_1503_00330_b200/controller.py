@@ -72,6 +72,14 @@ class ControlPlan:
     def replaced(self, controls) -> "ControlPlan":
         return ControlPlan(np.asarray(controls, float), self.dt, self.origin_time, self.lo, self.hi)
 
+    @classmethod
+    def _clipped(cls, controls, dt, origin_time, lo, hi) -> "ControlPlan":
+        """A plan from (N, 4) float64 controls already inside [lo, hi] (the device update
+        clips), skipping the constructor's re-clip."""
+        p = cls.__new__(cls)
+        p.controls, p.dt, p.origin_time, p.lo, p.hi = controls, dt, origin_time, lo, hi
+        return p
+
 
 @dataclass
 class PiConfig:
@@ -185,6 +193,7 @@ class RolloutEngine:
         self.noise = noise
         self.use_graph = bool(use_graph)
         self._ctxs: dict[tuple[int, int], _abi.Context] = {}
+        self._bound: dict[int, tuple] = {}  # per context: key of the dynamics + cost last bound
 
     def context(self, num_rollouts: int, horizon: int) -> "_abi.Context":
         key = (int(num_rollouts), int(horizon))
@@ -204,8 +213,18 @@ class RolloutEngine:
         return ctx
 
     def _bind(self, ctx, plan, cost_model) -> None:
+        """Stage the dynamics constants and the cost plugin; skipped when both are unchanged
+        since the last call on this context (compared by value, so mutating the plugin
+        between steps, e.g. switching waypoints, is picked up)."""
+        p = self.params
+        key = (p.mass, p.gravity, p.rate_gain, p.dt, np.asarray(plan.lo, float).tobytes(),
+               np.asarray(plan.hi, float).tobytes(), _cost_key(cost_model))
+        if key[-1] is not None and self._bound.get(id(ctx)) == key:
+            return
+        self._bound.pop(id(ctx), None)
         ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
         ctx.call("pi2_set_cost", cost_struct(cost_model))
+        self._bound[id(ctx)] = key
 
     def evaluate(self, state: QuadState, plan: ControlPlan, noise, cost_model,
                  dyn_noise=None) -> RolloutBatch:
@@ -242,6 +261,35 @@ class RolloutEngine:
         ctx.call("pi2_optimize", _abi.ptr(np.ascontiguousarray(state.as_array())), _abi.ptr(controls),
                  optimize_args(cfg, cycle_index, self.use_graph))
         return plan.replaced(controls)
+
+
+    def receding_device(self, state: QuadState, plan: ControlPlan, cost_model, cycle_index: int = 0):
+        """``receding_horizon_step`` on the GPU with device noise: optimise, then take the
+        first control and shift the plan inside the C ABI (pi2_receding_horizon_step)."""
+        cfg = self.config
+        if cfg.iterations_per_step > _abi.MAX_ITERATIONS:
+            raise ValueError(f"iterations_per_step must be <= {_abi.MAX_ITERATIONS} on the device path")
+        ctx = self.context(cfg.num_rollouts, len(plan))
+        self._bind(ctx, plan, cost_model)
+        controls = np.array(plan.controls, dtype=np.float64, order="C")
+        first = np.empty(4)
+        ctx.call("pi2_receding_horizon_step", _abi.ptr(np.ascontiguousarray(state.as_array())),
+                 _abi.ptr(controls), optimize_args(cfg, cycle_index, self.use_graph), _abi.ptr(first))
+        return (Control(first[:3].copy(), float(first[3])),
+                ControlPlan._clipped(controls, plan.dt, plan.origin_time + plan.dt, plan.lo, plan.hi))
+
+
+def _cost_key(cost_model):
+    """Value key of a cost plugin's device descriptor (see simworld.cost_struct); None when
+    the plugin has no device form (cost_struct then raises)."""
+    if all(hasattr(cost_model, a) for a in ("waypoint", "obstacles", "z_floor", "lo", "hi")):
+        f32 = np.float32
+        return ("nav", np.asarray(cost_model.waypoint, f32).tobytes(), np.asarray(cost_model.obstacles, f32).tobytes(),
+                float(np.float32(cost_model.z_floor)), np.asarray(cost_model.lo, f32).tobytes(),
+                np.asarray(cost_model.hi, f32).tobytes())
+    if hasattr(cost_model, "threshold") and not hasattr(cost_model, "waypoint"):
+        return ("threshold", float(np.float32(cost_model.threshold)))
+    return None
 
 
 def optimize_args(cfg: PiConfig, cycle_index: int, use_graph: bool = True) -> "_abi.OptimizeArgs":
@@ -309,5 +357,7 @@ def optimize(state: QuadState, plan: ControlPlan, config: PiConfig, model, cost_
 def receding_horizon_step(state: QuadState, plan: ControlPlan, config: PiConfig, model, cost_model,
                           cycle_index: int = 0, engine: RolloutEngine | None = None):
     """Optimise; return the first control and the shifted plan (controller.py:398-413)."""
+    if engine is not None and engine.noise == "device" and engine.config is config:
+        return engine.receding_device(state, plan, cost_model, cycle_index)
     optimized = optimize(state, plan, config, model, cost_model, cycle_index, engine)
     return optimized.control_at(0), optimized.shifted()

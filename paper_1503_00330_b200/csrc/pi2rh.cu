@@ -54,7 +54,9 @@ struct pi2_ctx {
   size_t tc_cap = 0;
   int tc_smem = 0;
 
-  // device workspaces (sized by dims)
+  // device workspaces (sized by dims); StepArgs and the plan share one block (d_io)
+  // so that one copy stages both
+  uint8_t *d_io = nullptr;
   StepArgs *d_args = nullptr;
   double *d_plan = nullptr, *d_plan2 = nullptr;
   float4 *d_xin = nullptr, *d_ang_last = nullptr, *d_lw = nullptr;  // d_lw: mean rows then std rows
@@ -70,14 +72,16 @@ struct pi2_ctx {
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
 
-  // pinned staging
+  // pinned staging, same layout as d_io
+  uint8_t *h_io = nullptr;
   StepArgs *h_args = nullptr;
   double *h_plan = nullptr;  // N x 4
 
-  // graph cache for pi2_optimize
-  cudaGraphExec_t graph = nullptr;
-  int graph_iters = -1;
-  double graph_neg_inv = 0.0;
+  // graph cache: `graph` = the iterations (pi2_iterate_device); `graph_io` = H2D of
+  // StepArgs + plan, the iterations, D2H of the plan (pi2_optimize)
+  cudaGraphExec_t graph = nullptr, graph_io = nullptr;
+  int graph_iters = -1, graph_io_iters = -1;
+  double graph_neg_inv = 0.0, graph_io_neg_inv = 0.0;
 
   int smem_optin = 0;
 };
@@ -129,9 +133,13 @@ int bind(pi2_ctx *ctx) {
 
 void invalidate_graph(pi2_ctx *ctx) {
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-  ctx->graph = nullptr;
-  ctx->graph_iters = -1;
+  if (ctx->graph_io) cudaGraphExecDestroy(ctx->graph_io);
+  ctx->graph = ctx->graph_io = nullptr;
+  ctx->graph_iters = ctx->graph_io_iters = -1;
 }
+
+// StepArgs is padded to this in the d_io / h_io blocks (the plan follows)
+constexpr size_t kIoArgsBytes = (sizeof(StepArgs) + 255) / 256 * 256;
 
 int ensure_params(pi2_ctx *ctx) {
   if (!ctx->params_dirty) return PI2_OK;
@@ -336,9 +344,9 @@ int check_ready(pi2_ctx *ctx) {
 }
 
 // Fill the pinned StepArgs and queue its H2D copy (waits for the previous one).
-int stage_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, double ceiling,
-               cudaStream_t st) {
-  CU(cudaEventSynchronize(ctx->staged));
+// host side of stage_args: state, cost, keys into the pinned StepArgs (caller has
+// waited for ctx->staged)
+void fill_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, double ceiling) {
   StepArgs &h = *ctx->h_args;
   if (state) std::memcpy(h.state, state, sizeof h.state);
   h.cost = ctx->cost;
@@ -352,6 +360,12 @@ int stage_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, 
       derive_key(opt->seed, PI2_STREAM_DYNAMICS, opt->cycle, (uint64_t)it, h.keys[it][1]);
     }
   }
+}
+
+int stage_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, double ceiling,
+               cudaStream_t st) {
+  CU(cudaEventSynchronize(ctx->staged));
+  fill_args(ctx, state, opt, ceiling);
   CU(cudaMemcpyAsync(ctx->d_args, ctx->h_args, sizeof(StepArgs), cudaMemcpyHostToDevice, st));
   CU(cudaEventRecord(ctx->staged, st));
   return PI2_OK;
@@ -547,8 +561,9 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
     g_noctx_err = "device allocation failed: " #p;                                    \
     return cleanup(PI2_ERR_OOM);                                                      \
   }
-  ALLOC(ctx->d_args, sizeof(StepArgs));
-  ALLOC(ctx->d_plan, sizeof(double) * 4 * N);
+  ALLOC(ctx->d_io, kIoArgsBytes + sizeof(double) * 4 * N);
+  ctx->d_args = reinterpret_cast<StepArgs *>(ctx->d_io);
+  ctx->d_plan = reinterpret_cast<double *>(ctx->d_io + kIoArgsBytes);
   ALLOC(ctx->d_plan2, sizeof(double) * 4 * N);
   ALLOC(ctx->d_xin, sizeof(float4) * K * N);
   ALLOC(ctx->d_ang_last, sizeof(float4) * K);
@@ -560,12 +575,13 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming) != cudaSuccess ||
-      cudaMallocHost((void **)&ctx->h_args, sizeof(StepArgs)) != cudaSuccess ||
-      cudaMallocHost((void **)&ctx->h_plan, sizeof(double) * 4 * N) != cudaSuccess) {
+      cudaMallocHost((void **)&ctx->h_io, kIoArgsBytes + sizeof(double) * 4 * N) != cudaSuccess) {
     cudaGetLastError();
     g_noctx_err = "stream/event/pinned allocation failed";
     return cleanup(PI2_ERR_CUDA);
   }
+  ctx->h_args = reinterpret_cast<StepArgs *>(ctx->h_io);
+  ctx->h_plan = reinterpret_cast<double *>(ctx->h_io + kIoArgsBytes);
   std::memset(ctx->h_args, 0, sizeof(StepArgs));
   ctx->h_args->neg_inv_temp = -1.0;
   ctx->h_args->ceiling = 1e8;
@@ -579,13 +595,12 @@ void pi2_destroy(pi2_ctx *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   invalidate_graph(ctx);
-  void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_args,   ctx->d_plan,  ctx->d_plan2,    ctx->d_xin,
+  void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_io,     ctx->d_plan2,    ctx->d_xin,
                   ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
                   ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch};
   for (void *p : bufs)
     if (p) cudaFree(p);
-  if (ctx->h_args) cudaFreeHost(ctx->h_args);
-  if (ctx->h_plan) cudaFreeHost(ctx->h_plan);
+  if (ctx->h_io) cudaFreeHost(ctx->h_io);
   if (ctx->staged) cudaEventDestroy(ctx->staged);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   cudaGetLastError();
@@ -761,33 +776,42 @@ int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const dou
 // All iterations of a step on the device plan: eager, or one cached CUDA graph
 // (kernel arguments are fixed pointers; per-call state, keys and cost come
 // from the staged StepArgs, so replays need no re-capture).
-static int run_iterations(pi2_ctx *ctx, const pi2_optimize_args *args, cudaStream_t st) {
+// io: also copy StepArgs + plan in from the pinned block first and the plan back out last
+static int enqueue_iterations(pi2_ctx *ctx, int iterations, double neg_inv, bool io, cudaStream_t st) {
+  const size_t plan_bytes = sizeof(double) * 4 * ctx->N;
+  if (io) CU(cudaMemcpyAsync(ctx->d_io, ctx->h_io, kIoArgsBytes + plan_bytes, cudaMemcpyHostToDevice, st));
+  for (int it = 0; it < iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
+  if (io) CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, plan_bytes, cudaMemcpyDeviceToHost, st));
+  return PI2_OK;
+}
+
+static int run_iterations(pi2_ctx *ctx, const pi2_optimize_args *args, cudaStream_t st, bool io = false) {
   const double neg_inv = -1.0 / args->temperature;
-  if (!args->use_graph) {
-    for (int it = 0; it < args->iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
-    return PI2_OK;
-  }
-  if (!(ctx->graph && ctx->graph_iters == args->iterations && ctx->graph_neg_inv == neg_inv)) {
-    invalidate_graph(ctx);
+  if (!args->use_graph) return enqueue_iterations(ctx, args->iterations, neg_inv, io, st);
+  cudaGraphExec_t &exec = io ? ctx->graph_io : ctx->graph;
+  int &iters = io ? ctx->graph_io_iters : ctx->graph_iters;
+  double &ninv = io ? ctx->graph_io_neg_inv : ctx->graph_neg_inv;
+  if (!(exec && iters == args->iterations && ninv == neg_inv)) {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    iters = -1;
     // capture on the private stream (never a caller's), ordered after `st` by the launch below
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = PI2_OK;
-    for (int it = 0; it < args->iterations && rc == PI2_OK; ++it)
-      rc = launch_iteration(ctx, it, neg_inv, nullptr, true, ctx->stream);
+    const int rc = enqueue_iterations(ctx, args->iterations, neg_inv, io, ctx->stream);
     const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
     if (rc != PI2_OK) {
       if (g) cudaGraphDestroy(g);
       return rc;
     }
     if (ec != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
-    const cudaError_t ei = cudaGraphInstantiate(&ctx->graph, g, 0);
+    const cudaError_t ei = cudaGraphInstantiate(&exec, g, 0);
     cudaGraphDestroy(g);
     if (ei != cudaSuccess) return fail(ctx, PI2_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
-    ctx->graph_iters = args->iterations;
-    ctx->graph_neg_inv = neg_inv;
+    iters = args->iterations;
+    ninv = neg_inv;
   }
-  CU(cudaGraphLaunch(ctx->graph, st));
+  CU(cudaGraphLaunch(exec, st));
   return PI2_OK;
 }
 
@@ -810,11 +834,11 @@ int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi
   if (args->iterations == 0) return PI2_OK;  // plan unchanged (test_controller.py:261-265)
   cudaStream_t st = ctx->stream;
   TRY(ensure_params(ctx));
-  TRY(stage_args(ctx, state, args, args->cost_ceiling, st));
+  // one graph launch: H2D of StepArgs + plan, the iterations, D2H of the plan
+  CU(cudaEventSynchronize(ctx->staged));
+  fill_args(ctx, state, args, args->cost_ceiling);
   std::memcpy(ctx->h_plan, plan_inout, sizeof(double) * 4 * ctx->N);
-  CU(cudaMemcpyAsync(ctx->d_plan, ctx->h_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyHostToDevice, st));
-  TRY(run_iterations(ctx, args, st));
-  CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost, st));
+  TRY(run_iterations(ctx, args, st, true));
   CU(cudaStreamSynchronize(st));
   std::memcpy(plan_inout, ctx->h_plan, sizeof(double) * 4 * ctx->N);
   return PI2_OK;

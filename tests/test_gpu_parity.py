@@ -335,6 +335,35 @@ def test_graph_replay_matches_eager_and_is_deterministic():
     np.testing.assert_array_equal(outs[0].controls, e.optimize_device(state, plan, cost, 0).controls)
 
 
+def test_receding_fast_path_equals_optimize_then_shift():
+    """receding_horizon_step on a device engine (pi2_receding_horizon_step, cached plugin
+    binding) == optimize_device + control_at(0) + shifted(), bitwise, across a waypoint
+    switch (the binding cache must notice the new cost) and with iterations_per_step=0."""
+    params, model, cfg, task, state, plan, cost = _device_setup(iters=1)
+    fast = P.RolloutEngine(model, cfg, device=0, noise="device")
+    slow = P.RolloutEngine(model, cfg, device=0, noise="device")
+    p_fast = p_slow = plan
+    for cycle, wp in enumerate((1, 1, 2, 2, 1)):
+        c = P.RolloutCost(task, wp)
+        ctrl, p_fast = P.receding_horizon_step(state, p_fast, cfg, model, c, cycle, fast)
+        opt = slow.optimize_device(state, p_slow, c, cycle)
+        want_ctrl, p_slow = opt.control_at(0), opt.shifted()
+        np.testing.assert_array_equal(ctrl.desired_rates, want_ctrl.desired_rates)
+        assert ctrl.thrust == want_ctrl.thrust
+        np.testing.assert_array_equal(p_fast.controls, p_slow.controls)
+        assert p_fast.origin_time == p_slow.origin_time
+    cost.waypoint = task.waypoints[2].astype(np.float32)  # mutate the plugin in place
+    a = P.receding_horizon_step(state, plan, cfg, model, cost, 9, fast)[1].controls
+    b = slow.optimize_device(state, plan, P.RolloutCost(task, 2), 9).shifted().controls
+    np.testing.assert_array_equal(a, b)
+    cfg0 = P.PiConfig(num_rollouts=cfg.num_rollouts, sub_rollouts=cfg.sub_rollouts,
+                      horizon_steps=cfg.horizon_steps, iterations_per_step=0)
+    e0 = P.RolloutEngine(model, cfg0, device=0, noise="device")
+    ctrl, shifted = P.receding_horizon_step(state, plan, cfg0, model, cost, 0, e0)
+    np.testing.assert_array_equal(shifted.controls, plan.shifted().controls)
+    assert ctrl.thrust == plan.controls[0, 3]
+
+
 def test_sharded_partials_are_gpu_count_invariant():
     """Rank shards evaluated one after another on one GPU (no cross-waiting kernels):
     the fixed-order combine gives the single-context plan bitwise for G = 2 and 4."""
