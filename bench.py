@@ -18,8 +18,11 @@ hybrid-LWPR model (paper_1503_00330_b200.synthetic), device-generated noise.
 * cpu_baseline / --impl reference: the reference algorithm (numpy oracle port,
   oracle/) on the host cores, on a bounded sample of the same workload.
 
-Under torchrun (N > 1) rollouts are sharded across ranks (strong scaling) and the
-per-timestep softmax partials are all-gathered over NCCL.
+Under torchrun (N > 1) rollouts are sharded across ranks and the per-timestep
+softmax partials are all-gathered over NCCL.  Default --scaling weak: every GPU
+keeps the named workload's K rollouts (K_total = K x N, the same control step
+with N times the samples at the same latency); --scaling strong splits the
+named K over the N GPUs (BASELINE C4's framing: K=2^20 on 8 GPUs).
 """
 
 from __future__ import annotations
@@ -51,6 +54,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="C2")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="N > 1: weak = K rollouts per GPU, strong = K rollouts in total")
     p.add_argument("--cpu-sample", type=int, default=4096, help="rollouts in the CPU baseline sample")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -229,6 +234,8 @@ def run_ours(args, rank: int, world: int, local: int):
             dist.init_process_group(backend)
     torch.cuda.set_device(local)
     cfgd, desc = workload(args.config)
+    if args.scaling == "weak":
+        cfgd["K"] *= world
     K, T, L, M = cfgd["K"], cfgd["T"], cfgd["L"], cfgd["M"]
     params = P.QuadParams()
     model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=0), params)
@@ -351,13 +358,14 @@ def run_ours(args, rank: int, world: int, local: int):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f32 (LWPR, integration, cost) + f64 (attitude, cost-to-go, update)",
         "data": "synthetic (seeded hybrid-LWPR model linearising the rigid-body quadrotor; device Philox noise)",
         "config": {
-            "workload": f"{args.config}: {desc}",
-            "K": K, "T": T, "L": L, "M": M, "iterations_per_step": 1,
+            "workload": f"{args.config}: {desc}" + (f" (x{world} GPUs, weak scaling: K per GPU)"
+                                                    if world > 1 and args.scaling == "weak" else ""),
+            "K": K, "K_per_gpu": k_local, "T": T, "L": L, "M": M, "iterations_per_step": 1,
             "parallelism": f"rollouts sharded over {world} GPU(s)",
             "l2": "working set > L2 (xin+LWPR rows+costs ≈ %.0f MB per GPU)" % ((k_local * T * (16 + 32 + 8)) / 1e6),
         },
@@ -411,8 +419,10 @@ def run_ours(args, rank: int, world: int, local: int):
     return line
 
 
-def run_reference(args):
+def run_reference(args, world: int = 1):
     cfgd, desc = workload(args.config)
+    if args.scaling == "weak":
+        cfgd["K"] *= world  # the same config as our arm; the CPU sample below is bounded anyway
     cb = cpu_reference(cfgd, args.cpu_sample, 0.0, max_steps=args.warmup + args.steps)
     times = cb.pop("step_times_s")[args.warmup:] or [cb["ms_per_step"] / 1e3]
     step = sum(times) / len(times)
@@ -428,7 +438,7 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": step * 1e3,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f32 + f64 (numpy)",
         "data": "synthetic",
@@ -445,7 +455,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args)), flush=True)
+            print(json.dumps(run_reference(args, world)), flush=True)
         return 0
     line = run_ours(args, rank, world, local)
     if line is not None:
