@@ -564,18 +564,30 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
     for (int c = 0; c < 3; ++c) cs[m][c] = ccs[m][c] = -0.0f;  // -0 + x == x: cumsum start
   }
 
+  // the rows of step t + 1 are loaded while step t computes (hides HBM latency);
+  // the analytic model's input row of step t + 1 is this step's post-step attitude row
+  const bool hybrid = model == PI2_MODEL_HYBRID_LWPR;
+  const bool with_std = hybrid && a.spread;
+  float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n;
+  if (hybrid) m4n = __ldg(a.lw_mean + k);
+  if (with_std) s4n = __ldg(a.lw_std + k);
+  float4 apn = (1 < N) ? __ldg(a.xin + a.K + k) : __ldg(a.ang_last + k);
+  float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldg(a.xin + k) : m4n;
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
+    const float4 m4 = m4n, s4 = s4n, ap = apn;
+    if (t + 1 < N) {
+      if (hybrid) m4n = __ldg(a.lw_mean + row + a.K);
+      if (with_std) s4n = __ldg(a.lw_std + row + a.K);
+      apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + k);
+    }
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
-    if (model == PI2_MODEL_HYBRID_LWPR) {
-      const float4 m4 = a.lw_mean[row];
+    if (hybrid) {
       mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
       if (a.spread) {
-        const float4 s4 = a.lw_std[row];
         sd[0] = s4.x; sd[1] = s4.y; sd[2] = s4.z;
       }
     } else if (model == PI2_MODEL_ANALYTIC) {  // dynamics.py:175-185
-      const float4 xr = a.xin[row];
       float sr, cr, sp, cp, sy, cy;
       sincosf(xr.x, &sr, &cr);
       sincosf(xr.y, &sp, &cp);
@@ -589,9 +601,12 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       mn[0] = mn[1] = mn[2] = 0.0f;
       sd[2] = a.two_point;
     }
-    const float4 ap = (t + 1 < N) ? a.xin[row + a.K] : a.ang_last[k];  // post-step attitude
-    const float angterm = __fmul_rn(
+    float angterm = __fmul_rn(
         __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
+    // consume the finite pad lanes so ptxas keeps the in-flight prefetch registers (see
+    // rollout_group_kernel)
+    angterm = fmaf(__fadd_rn(__fadd_rn(m4.w, s4.w), ap.w), 0.0f, angterm);
+    xr = ap;  // the analytic model's input row of step t + 1
     const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
     float q[MCAP];
 #pragma unroll
@@ -743,8 +758,12 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
         mn[0] = mn[1] = mn[2] = 0.0f;
         sd[2] = a.two_point;
       }
-      const float angterm = __fmul_rn(
+      float angterm = __fmul_rn(
           __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
+      // consume the (finite) pad lanes of the prefetched rows: an unused .w lets ptxas
+      // reuse that register while the next step's 128-bit load is still in flight, a
+      // write-after-write stall of a full DRAM latency per step (ncu, rollout kernel)
+      angterm = fmaf(__fadd_rn(__fadd_rn(m4.w, s4.w), ap.w), 0.0f, angterm);
       const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
       float d[3];
       if (device_dyn) {
