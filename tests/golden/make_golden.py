@@ -128,7 +128,7 @@ def make_lwpr():
 
 
 def evaluate_case(name, stacks, K, N, M, seed, cycle, waypoint, state_pos=None,
-                  plan_thrust=None, chunk=7, std=(2.0, 2.0, 0.8, 0.05)):
+                  plan_thrust=None, chunk=7, std=(2.0, 2.0, 0.8, 0.05), plant=None):
     p = D.QuadParams()
     model = D.AnalyticModel(p) if stacks is None else ref_hybrid(stacks)
     task = S.Task.default()
@@ -139,10 +139,13 @@ def evaluate_case(name, stacks, K, N, M, seed, cycle, waypoint, state_pos=None,
     if plan_thrust is not None:
         plan = plan.replaced(np.tile([0.0, 0.0, 0.0, plan_thrust], (N, 1)))
     noise = C.sample_noise(cfg, cycle, 0)
+    for (k, t, c), v in (plant or {}).items():  # non-finite exploration samples
+        noise[k, t, c] = v
     engine = C.RolloutEngine(model, cfg)
     dyn = C.sample_dynamics_noise(cfg, cycle, 0) if engine.use_spread else None
-    batch = engine.evaluate(state, plan, noise, S.RolloutCost(task, waypoint), dyn)
-    new_plan = C.path_integral_update(plan, batch, cfg.temperature)
+    with np.errstate(invalid="ignore", over="ignore"):
+        batch = engine.evaluate(state, plan, noise, S.RolloutCost(task, waypoint), dyn)
+        new_plan = C.path_integral_update(plan, batch, cfg.temperature)
     arrays = dict(
         K=np.array(K), N=np.array(N), M=np.array(M), seed=np.array(seed), cycle=np.array(cycle),
         waypoint_index=np.array(waypoint), analytic=np.array(stacks is None),
@@ -181,6 +184,23 @@ def make_eval():
                       seed=10, cycle=0, waypoint=0, state_pos=np.array([-1.1, -0.9, 0.3]),
                       plan_thrust=0.175)
     print("crash_m1: crashed", int(b.crash_flags.sum()))
+    make_nonfinite()
+
+
+NONFINITE = {(1, 3, 0): np.nan, (2, 0, 3): np.inf, (3, 5, 1): -np.inf, (5, 9, 2): np.nan,
+             (6, 11, 3): np.nan, (7, 2, 0): np.inf}
+
+
+def make_nonfinite():
+    """NaN / +-inf exploration samples: the clip keeps NaN and saturates +-inf
+    (controller.py:259), NaN rollouts take the cost ceiling and the crash flag
+    (:243-246), and the update's sum over the raw noise turns NaN / inf into a
+    NaN or saturated plan entry (:368-371)."""
+    for name, m, stacks in (("nonfinite_m1", 1, synthetic.hybrid_stacks(16, seed=11)),
+                            ("nonfinite_m4", 4, synthetic.hybrid_stacks(12, seed=12))):
+        b = evaluate_case(name, stacks, K=40, N=14, M=m, seed=13, cycle=0, waypoint=1, plant=NONFINITE)
+        print(name, "ceiling rollouts", int((b.costs_to_go == 1e8).all(axis=1).sum()),
+              "crashed", int(b.crash_flags.sum()))
 
 
 def make_update():
@@ -289,6 +309,9 @@ def make_trial():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["nonfinite"]:
+        make_nonfinite()
+        sys.exit(0)
     make_rng()
     make_lwpr()
     make_eval()

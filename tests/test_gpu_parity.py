@@ -27,7 +27,11 @@ def cost_rel_err(got, want):
 
 
 def du_err(new, want, plan):
-    du, wdu = new - plan, want - plan
+    """Per-channel max |Δu error| / max |Δu|; NaN plan entries (NaN exploration noise,
+    controller.py:368-371) must sit at the same places and are excluded."""
+    np.testing.assert_array_equal(np.isnan(new), np.isnan(want))
+    ok = ~np.isnan(want)
+    du, wdu = np.where(ok, new - plan, 0.0), np.where(ok, want - plan, 0.0)
     scale = np.maximum(np.max(np.abs(wdu), axis=0), 1e-300)
     return np.max(np.abs(du - wdu), axis=0) / scale
 
