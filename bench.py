@@ -342,7 +342,8 @@ def run_ours(args, rank: int, world: int, local: int):
     lwpr_flops = rows * 3 * L * flops_per_field
     achieved = lwpr_flops / (stages["lwpr"] / 1e3) / 1e12
     # which LWPR kernel ran: the tcgen05 one for the variance path unless disabled
-    tc = M > 1 and os.environ.get("PI2_LWPR_TC", "1") != "0"
+    tc_mode = os.environ.get("PI2_LWPR_TC", "1")  # see tc_wanted in csrc/pi2rh.cu
+    tc = tc_mode == "1" or (tc_mode == "2" and M > 1)
     exps = rows * 3 * L  # one MUFU ex2 per (row, axis, field)
     mufu_peak = float(peaks.get("mufu_ex2_per_s", 4.60e12))
     clk = clocks.summary()

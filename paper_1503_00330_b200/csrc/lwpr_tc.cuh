@@ -379,7 +379,11 @@ inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, Lwpr
     for (double &v : gs) v /= a.L;
     ta.axis_off[ax] = w_floats;
     ta.nchunks[ax] = (a.L + kTcChunk - 1) / kTcChunk;
+#ifdef PI2_TC_EVEN_SPLIT
     const int per = (a.L + ta.nchunks[ax] - 1) / ta.nchunks[ax];  // even split, e.g. 100 -> 50 + 50
+#else
+    const int per = kTcChunk;  // full chunks, then the remainder: 100 -> 64 + 36 (padded 104, not 112)
+#endif
     for (int c = 0; c < ta.nchunks[ax]; ++c) {
       const int l0 = c * per, n = std::min(per, a.L - l0);
       const int lc = (n + 7) / 8 * 8;
@@ -414,7 +418,6 @@ inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, Lwpr
       blob.insert(blob.end(), lo.begin(), lo.end());
       w_floats += (int64_t)hi.size() + (int64_t)lo.size();
       for (int j = 0; j < kTcChunk; ++j) lvs.push_back(j < n ? (float)a.lvar[l0 + j] : 0.0f);
-      (void)per;
     }
   }
   ta.w_floats = w_floats;

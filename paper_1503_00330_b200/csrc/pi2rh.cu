@@ -49,6 +49,7 @@ struct pi2_ctx {
   // tensor-core LWPR operands (shared-metric models, lwpr_tc.cuh)
   bool tc_ok = false;
   bool tc_enabled = true;  // PI2_LWPR_TC=0 forces the CUDA-core kernel
+  int tc_mode = 1;         // see tc_wanted
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -197,6 +198,10 @@ int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st) {
   return PI2_OK;
 }
 
+// PI2_LWPR_TC: unset / 1 = tensor cores for every eligible launch, 2 = variance path
+// only, 0 = never
+bool tc_wanted(const pi2_ctx *ctx, bool var) { return ctx->tc_mode == 1 || (ctx->tc_mode == 2 && var); }
+
 template <bool VAR>
 int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out, float *sd_out, cudaStream_t st) {
   LwprTcArgs a = ctx->tc;
@@ -221,11 +226,11 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
 int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
                 float *sd_out, int stride, int sqrt_out, cudaStream_t st) {
   TRY(ensure_params(ctx));
-  // all three axes with variance into float4 rows (the sub-rollout path): tensor
-  // cores when eligible.  Measured on B200 (profiles/README.md): 491 vs 510 us at
-  // C2; the mean-only CUDA-core loop (10 FMA-pipe ops/field) stays faster.
-  if (ctx->tc_ok && sd_out && a_begin == 0 && a_end == 3 && stride == 4 && sqrt_out)
-    return launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st);
+  // all three axes into float4 rows (the rollout path): tensor cores when eligible
+  // (shared metric, each axis' weights fit at full residency; PI2_LWPR_TC=0 disables)
+  if (ctx->tc_ok && tc_wanted(ctx, sd_out != nullptr) && a_begin == 0 && a_end == 3 && stride == 4 && sqrt_out)
+    return sd_out ? launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st)
+                  : launch_lwpr_tc<false>(ctx, rows, x, mean_out, nullptr, st);
   LwprArgs a{};
   a.params = ctx->d_params;
   for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
@@ -552,7 +557,10 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   };
   if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  if (const char *e = getenv("PI2_LWPR_TC")) ctx->tc_enabled = std::atoi(e) != 0;
+  if (const char *e = getenv("PI2_LWPR_TC")) {
+    ctx->tc_mode = std::atoi(e);
+    ctx->tc_enabled = ctx->tc_mode != 0;
+  }
   const int64_t K = ctx->K, N = ctx->N;
   ctx->n_chunks = (K + kChunk - 1) / kChunk;
 #define ALLOC(p, bytes)                                                               \
