@@ -342,14 +342,37 @@ def run_ours(args, rank: int, world: int, local: int):
     lwpr_flops = rows * 3 * L * flops_per_field
     achieved = lwpr_flops / (stages["lwpr"] / 1e3) / 1e12
     # which LWPR kernel ran: the tcgen05 one for the variance path unless disabled
-    tc_mode = os.environ.get("PI2_LWPR_TC", "1")  # see tc_wanted in csrc/pi2rh.cu
-    tc = tc_mode == "1" or (tc_mode == "2" and M > 1)
-    exps = rows * 3 * L  # one MUFU ex2 per (row, axis, field)
+    # which LWPR kernel ran, and the share of its 2^x on MUFU (the rest on the FMA pipe)
+    kern, share = _abi.C.c_int32(), _abi.C.c_double()
+    ctx.call("pi2_lwpr_kernel", int(M > 1), _abi.C.byref(kern), _abi.C.byref(share))
+    tc = kern.value == 1
+    exps = rows * 3 * L  # one 2^x per (row, axis, field)
     mufu_peak = float(peaks.get("mufu_ex2_per_s", 4.60e12))
+    lw_s = stages["lwpr"] / 1e3
     clk = clocks.summary()
     peak_obs = n_sm * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12 if clk.get("sm_mhz") else None
     h2d = 12 * 8 + T * 4 * 8 + 8 * (12 + 4 * 16 + 4 + 2) + 4 * 48  # state + plan + StepArgs
     d2h = T * 4 * 8
+    fp32 = {
+        "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved / peak_tflops,
+        "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json)",
+        "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
+        "flops_per_launch": lwpr_flops, "flops_per_field": flops_per_field,
+    }
+    mufu = {"ex2_per_launch": exps, "mufu_share": share.value,
+            "achieved": exps * share.value / lw_s / 1e12, "peak": mufu_peak / 1e12, "unit": "Tex2/s",
+            "frac": exps * share.value / lw_s / mufu_peak,
+            "peak_source": "profiles/micro/mufu_mix_b200.txt (MUFU-only ex2 stream, 148 SMs)"}
+    if tc:  # binding unit: MUFU (the linear parts are on the tensor cores)
+        roofline = {"bound": "mufu", "kernel": "lwpr_tc_kernel (tcgen05 3xTF32 field GEMM + exp/moments)",
+                    **{k: mufu[k] for k in ("achieved", "peak", "unit", "frac", "peak_source")},
+                    "ex2_per_launch": exps, "mufu_share": share.value,
+                    "traffic": lwpr_traffic(args.config, tc) if world == 1 else None,
+                    "fp32_equivalent": {**fp32, "note": "the same algorithmic FLOPs against the FP32 CUDA-core "
+                                        "peak; above 1 when the tensor cores carry the linear parts"}}
+    else:
+        roofline = {"bound": "fp32", "kernel": "lwpr_kernel (CUDA cores, FFMA2)", **fp32,
+                    "traffic": lwpr_traffic(args.config, tc) if world == 1 else None, "mufu": mufu}
     line = {
         "metric": METRIC,
         "value": value,
@@ -379,23 +402,7 @@ def run_ours(args, rank: int, world: int, local: int):
                    else "distributed.ShardedEngine.optimize",
         },
         "latency_ms": {"p50": p50, "p99": p99, "what": "e2e control step (host state/plan -> control)"},
-        "roofline": {
-            "bound": "fp32",
-            "kernel": "lwpr_tc_kernel (tcgen05 3xTF32 field GEMM + CUDA-core exp/moments)" if tc
-                      else "lwpr_kernel (CUDA cores, FFMA2)",
-            "achieved": achieved,
-            "peak": peak_tflops,
-            "unit": "TFLOP/s",
-            "frac": achieved / peak_tflops,
-            "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {sm_max:.0f} (MEASURED_PEAKS.json)",
-            "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
-            "flops_per_launch": lwpr_flops,
-            "flops_per_field": flops_per_field,
-            "traffic": lwpr_traffic(args.config, tc) if world == 1 else None,
-            "mufu": {"ex2_per_launch": exps, "achieved_per_s": exps / (stages["lwpr"] / 1e3),
-                     "peak_per_s": mufu_peak, "frac": exps / (stages["lwpr"] / 1e3) / mufu_peak,
-                     "peak_source": "profiles/micro/mufu_mix_b200.txt (MUFU-only ex2 stream)"},
-        },
+        "roofline": roofline,
         "stages_ms": stages,
         "clocks": clk,
         "gpu_launches": args.steps * (KERNELS_PER_ITER + (1 if world > 1 else 0)),

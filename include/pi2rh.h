@@ -196,6 +196,14 @@ int64_t pi2_partial_chunk(void); /* rollouts per leaf partial */
  * averaged over `reps` (plan not updated).  stage_ms[5] = attitude, LWPR,
  * rollout/cost, partials, combine (ms). */
 int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms);
+/* Which LWPR kernel the rollout path of this context runs for the staged
+ * model (variance != 0: the sub-rollout path with standard deviations):
+ * *kernel_out = PI2_LWPR_CUDA_CORES or PI2_LWPR_TENSOR_CORES; *mufu_share
+ * (may be NULL) = fraction of its 2^x evaluated on the MUFU unit (the rest
+ * on the FMA pipe).  Benchmark introspection. */
+#define PI2_LWPR_CUDA_CORES 0
+#define PI2_LWPR_TENSOR_CORES 1
+int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double *mufu_share);
 
 /* ---- noise / LWPR building blocks ------------------------------------- */
 /* Device noise for stream (seed, stream_id, cycle, iteration): control

@@ -133,13 +133,46 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 #define PI2_TC_T(i)
 #endif
 
-// 8 fields of one row: e = 2^logit, moments on field pairs
+#ifndef PI2_TC_POLY_VAR
+#define PI2_TC_POLY_VAR 0   // field pairs (of 4 per 8-field batch) whose 2^x runs on the FMA pipe:
+                            // the variance loop already loads the FMA pipe (1: +10 %), the mean-only
+                            // loop gains from 1 (L=100 380 -> 359 us, L=200 694 -> 637 us; 2: slower)
+#endif
+#ifndef PI2_TC_POLY_MEAN
+#define PI2_TC_POLY_MEAN 1
+#endif
+
+// 2^x of a field pair on the FMA pipe (FlashAttention-4's MUFU offload): x = n + f,
+// n = rint(x) via the 1.5 * 2^23 shift, f in [-1/2, 1/2]; 2^f by a degree-5
+// near-minimax polynomial (max rel. error 2.1e-7 in fp32 Horner, on par with
+// ex2.approx); 2^n enters as n << 23 added to the result's bits (one integer
+// multiply-add).  x >= -125 keeps 2^n normal: such weights are < 2^-61 of a row's
+// normaliser on the fast path (logits carry the +64 shift), and a row whose
+// weights all underflow takes the exact path either way.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x = make_float2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
+  const float2 t = __fadd2_rn(x, bc(12582912.0f));
+  const float2 n = __fadd2_rn(t, bc(-12582912.0f));
+  const float2 f = __ffma2_rn(n, bc(-1.0f), x);
+  float2 p = __ffma2_rn(bc(1.327645150013268e-03f), f, bc(9.675540961325169e-03f));
+  p = __ffma2_rn(p, f, bc(5.550713464617729e-02f));
+  p = __ffma2_rn(p, f, bc(2.402212023735046e-01f));
+  p = __ffma2_rn(p, f, bc(6.931469440460205e-01f));
+  p = __ffma2_rn(p, f, bc(1.000000119209290e+00f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y)));
+}
+
+// 8 fields of one row: e = 2^logit (the first POLY pairs on the FMA pipe, the rest
+// on MUFU), moments on field pairs
 template <bool VAR>
 __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *yy, const float *slv, float2 &den,
                                            float2 &num, float2 &m2, float2 &lv) {
+  constexpr int POLY = VAR ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN;
 #pragma unroll
   for (int i = 0; i < 8; i += 2) {
-    const float2 e = make_float2(ex2_ftz(__uint_as_float(lg[i])), ex2_ftz(__uint_as_float(lg[i + 1])));
+    const float2 x = make_float2(__uint_as_float(lg[i]), __uint_as_float(lg[i + 1]));
+    const float2 e = (i / 2 < POLY) ? exp2_poly2(x) : make_float2(ex2_ftz(x.x), ex2_ftz(x.y));
     const float2 y = make_float2(__uint_as_float(yy[i]), __uint_as_float(yy[i + 1]));
     den = __fadd2_rn(den, e);
     if (VAR) {

@@ -893,6 +893,18 @@ int pi2_iterate_local(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t itera
   return launch_iteration(ctx, iteration, -1.0 / args->temperature, root_dev, false, st);
 }
 
+int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double *mufu_share) {
+  TRY(check_ready(ctx));
+  if (!kernel_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(bind(ctx));
+  TRY(ensure_params(ctx));
+  const bool var = variance != 0;
+  const bool tc = ctx->tc_ok && tc_wanted(ctx, var);
+  *kernel_out = tc ? PI2_LWPR_TENSOR_CORES : PI2_LWPR_CUDA_CORES;
+  if (mufu_share) *mufu_share = tc ? 1.0 - (var ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN) / 4.0 : 1.0;
+  return PI2_OK;
+}
+
 int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms) {
   TRY(check_ready(ctx));
   TRY(bind(ctx));
