@@ -9,8 +9,8 @@
 // and field chunk (Lc <= 128 fields) puts both in TMEM.  The GEMM runs as
 // 3xTF32 (hi.hi + hi.lo + lo.hi, fp32 accumulate) — tests/test_tc_emulation.py
 // shows this keeps the LWPR mean within 1e-5 of the reference.  The CUDA cores
-// then only do  e = 2^logit (MUFU), den += e, num += e y', m2 += e y'^2,
-// lv += e var  on field pairs (FFMA2): the kernel becomes MUFU-bound.
+// then only do  e = 2^logit (MUFU), den += e, num += e y', m2 += e (y'^2 + var_l)
+// on field pairs (FFMA2): the kernel becomes MUFU-bound.
 //
 // tcgen05 usage: 1 CTA = 128 threads = 4 warps, warp w owns TMEM lanes
 // 32w..32w+31 = tile rows; thread 0 issues the 3 MMAs and commits to an
@@ -135,8 +135,8 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 
 #ifndef PI2_TC_POLY_VAR
 #define PI2_TC_POLY_VAR 0   // field pairs (of 4 per 8-field batch) whose 2^x runs on the FMA pipe:
-                            // the variance loop already loads the FMA pipe (1: +10 %), the mean-only
-                            // loop gains from 1 (L=100 380 -> 359 us, L=200 694 -> 637 us; 2: slower)
+                            // the variance loop slows down with any (1: 436 -> 456 us at L=100), the
+                            // mean-only loop gains from 1 (L=100 380 -> 359 us, L=200 694 -> 637 us)
 #endif
 #ifndef PI2_TC_POLY_MEAN
 #define PI2_TC_POLY_MEAN 1
@@ -175,11 +175,9 @@ __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *y
     const float2 e = (i / 2 < POLY) ? exp2_poly2(x) : make_float2(ex2_ftz(x.x), ex2_ftz(x.y));
     const float2 y = make_float2(__uint_as_float(yy[i]), __uint_as_float(yy[i + 1]));
     den = __fadd2_rn(den, e);
-    if (VAR) {
-      const float2 ey = __fmul2_rn(e, y);
-      num = __fadd2_rn(num, ey);
-      m2 = __ffma2_rn(ey, y, m2);
-      lv = __ffma2_rn(e, *reinterpret_cast<const float2 *>(slv + i), lv);
+    if (VAR) {  // second moment and local variances in one sum: e (y'^2 + var_l)
+      num = __ffma2_rn(e, y, num);
+      m2 = __ffma2_rn(e, __ffma2_rn(y, y, *reinterpret_cast<const float2 *>(slv + i)), m2);
     } else {
       num = __ffma2_rn(e, y, num);
     }
