@@ -141,6 +141,12 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 #ifndef PI2_TC_POLY_MEAN
 #define PI2_TC_POLY_MEAN 1
 #endif
+#ifndef PI2_TC_POLY_VAR_B  // the same for the second batch of each TMEM wait: one pair in 8
+#define PI2_TC_POLY_VAR_B 1  // for the variance loop (L=200 772 -> 759 us, L=100 435 -> 433 us)
+#endif
+#ifndef PI2_TC_POLY_MEAN_B
+#define PI2_TC_POLY_MEAN_B PI2_TC_POLY_MEAN
+#endif
 
 // 2^x of a field pair on the FMA pipe (FlashAttention-4's MUFU offload): x = n + f,
 // n = rint(x) via the 1.5 * 2^23 shift, f in [-1/2, 1/2]; 2^f by a degree-5
@@ -165,10 +171,10 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 
 // 8 fields of one row: e = 2^logit (the first POLY pairs on the FMA pipe, the rest
 // on MUFU), moments on field pairs
-template <bool VAR>
+template <bool VAR, bool SECOND = false>
 __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *yy, const float *slv, float2 &den,
                                            float2 &num, float2 &m2, float2 &lv) {
-  constexpr int POLY = VAR ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN;
+  constexpr int POLY = SECOND ? (VAR ? PI2_TC_POLY_VAR_B : PI2_TC_POLY_MEAN_B) : (VAR ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN);
 #pragma unroll
   for (int i = 0; i < 8; i += 2) {
     const float2 x = make_float2(__uint_as_float(lg[i]), __uint_as_float(lg[i + 1]));
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
         PI2_TMEM_WAIT16(la, ya);
         PI2_TMEM_WAIT16(lb, yb);
         tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
-        if (b + 1 < nb) tc_fields8<VAR>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+        if (b + 1 < nb) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
       }
       woff += (int64_t)2 * (2 * lc * 8);
       PI2_TC_T(3);

@@ -901,7 +901,9 @@ int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double 
   const bool var = variance != 0;
   const bool tc = ctx->tc_ok && tc_wanted(ctx, var);
   *kernel_out = tc ? PI2_LWPR_TENSOR_CORES : PI2_LWPR_CUDA_CORES;
-  if (mufu_share) *mufu_share = tc ? 1.0 - (var ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN) / 4.0 : 1.0;
+  if (mufu_share)  // field pairs on the FMA pipe, of 4 + 4 per two batches
+    *mufu_share = tc ? 1.0 - (var ? PI2_TC_POLY_VAR + PI2_TC_POLY_VAR_B : PI2_TC_POLY_MEAN + PI2_TC_POLY_MEAN_B) / 8.0
+                     : 1.0;
   return PI2_OK;
 }
 
