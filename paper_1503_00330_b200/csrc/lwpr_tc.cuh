@@ -196,11 +196,18 @@ __device__ __forceinline__ void tc_features(const AxisHeader &h, float4 x, uint8
   xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]), __fsub_rn(x.w, h.mu[3]));
   q = shared_qrow(h, xt);
   const float f[8] = {xt.x, xt.y, xt.z, xt.w, 1.0f, q, 0.0f, 0.0f};
+  float hi[8], lo[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float hi = tf32_rna(f[k]);
-    *reinterpret_cast<float *>(sa + umma_kmajor_off(r, k)) = hi;
-    *reinterpret_cast<float *>(sa + 4096 + umma_kmajor_off(r, k)) = tf32_rna(__fsub_rn(f[k], hi));
+    hi[k] = tf32_rna(f[k]);
+    lo[k] = tf32_rna(__fsub_rn(f[k], hi[k]));
+  }
+  // k = 0..3 and 4..7 of a row are 16 contiguous bytes each in the K-major layout:
+  // 4 conflict-free 128-bit stores instead of 16 4-way-conflicted 32-bit ones
+#pragma unroll
+  for (int k = 0; k < 8; k += 4) {
+    *reinterpret_cast<float4 *>(sa + umma_kmajor_off(r, k)) = make_float4(hi[k], hi[k + 1], hi[k + 2], hi[k + 3]);
+    *reinterpret_cast<float4 *>(sa + 4096 + umma_kmajor_off(r, k)) = make_float4(lo[k], lo[k + 1], lo[k + 2], lo[k + 3]);
   }
 }
 
@@ -211,10 +218,11 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
   if (row >= a.rows) return;
   const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
   float mean, var = 0.0f;
-  if (dn >= kSlowDen) {
-    const float mp = __fdiv_rn(nm, dn);
+  if (dn >= kSlowDen) {  // one correctly rounded reciprocal for both quotients
+    const float rd = __frcp_rn(dn);
+    const float mp = __fmul_rn(nm, rd);
     mean = __fadd_rn(gx, mp);
-    if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(m2, lv), dn), __fmul_rn(mp, mp)), 0.0f);
+    if (VAR) var = fmaxf(__fsub_rn(__fmul_rn(__fadd_rn(m2, lv), rd), __fmul_rn(mp, mp)), 0.0f);
   } else {
     lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
   }
