@@ -80,7 +80,9 @@ def test_evaluate_matches_reference_golden(name):
                                           (777, 20, 40, 3, True), (300, 10, 20, 16, False),
                                           (1, 1, 5, 1, False), (129, 7, 9, 8, False), (33, 70, 12, 1, False),
                                           (20000, 30, 24, 1, False), (20000, 24, 24, 4, False),
-                                          (17000, 20, 16, 3, True)])
+                                          (17000, 20, 16, 3, True),
+                                          # tensor-core LWPR chunking: 64 + 64 + 2 fields, one full chunk
+                                          (20000, 12, 130, 1, False), (17000, 10, 64, 4, False)])
 def test_evaluate_matches_oracle(K, N, L, M, full):
     stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
     params = P.QuadParams()
