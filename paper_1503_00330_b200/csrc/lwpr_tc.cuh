@@ -82,10 +82,31 @@ __device__ __forceinline__ uint32_t umma_idesc_tf32(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);            // M / 16
 }
 
+// tf32, round to nearest with ties away (cvt.rna.tf32.f32) for FINITE v, as two
+// integer ops: the conversion instruction shares the MUFU/XU pipe with the 2^x
+// flood of the co-resident warps and would queue behind it.  Non-finite rows
+// never use the result (tc_finalize sends them to the exact path).
 __device__ __forceinline__ float tf32_rna(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
+}
+
+// 1/d and sqrt(v) on the FMA pipe (MUFU is saturated by the 2^x of the other warps):
+// magic-constant seeds + Newton steps, relative error < 1e-7 for normal positive d
+// and v (B200-independent host emulation); callers route anything else (0,
+// denormals, inf, NaN) to the exact functions.
+__device__ __forceinline__ float rcp_fma(float d) {
+  float r = __uint_as_float(0x7EF311C3u - __float_as_uint(d));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r = __fmul_rn(r, __fmaf_rn(-d, r, 2.0f));
+  return __fmaf_rn(r, __fmaf_rn(-d, r, 1.0f), r);
+}
+__device__ __forceinline__ float sqrt_fma(float v) {
+  float y = __uint_as_float(0x5F3759DFu - (__float_as_uint(v) >> 1));  // ~ 1 / sqrt(v)
+  const float h = __fmul_rn(0.5f, v);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y = __fmul_rn(y, __fmaf_rn(-h, __fmul_rn(y, y), 1.5f));
+  const float s = __fmul_rn(v, y);  // sqrt(v), then one correction step
+  return v > 0.0f ? __fmaf_rn(__fmaf_rn(-s, s, v), __fmul_rn(0.5f, y), s) : 0.0f;
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, int acc) {
@@ -218,8 +239,10 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
   if (row >= a.rows) return;
   const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
   float mean, var = 0.0f;
-  if (dn >= kSlowDen) {  // one correctly rounded reciprocal for both quotients
-    const float rd = __frcp_rn(dn);
+  // fast path: a normal normaliser and finite inputs (non-finite rows follow the
+  // reference through the exact path)
+  if (dn >= kSlowDen && dn <= 3.0e38f && isfinite(__fadd_rn(__fadd_rn(xt.x, xt.y), __fadd_rn(__fadd_rn(xt.z, xt.w), q)))) {
+    const float rd = rcp_fma(dn);
     const float mp = __fmul_rn(nm, rd);
     mean = __fadd_rn(gx, mp);
     if (VAR) var = fmaxf(__fsub_rn(__fmul_rn(__fadd_rn(m2, lv), rd), __fmul_rn(mp, mp)), 0.0f);
@@ -227,7 +250,7 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
     lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
   }
   a.mean_out[row * 4 + ax] = mean;
-  if (VAR && a.sd_out) a.sd_out[row * 4 + ax] = a.sqrt_out ? __fsqrt_rn(var) : var;
+  if (VAR && a.sd_out) a.sd_out[row * 4 + ax] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
   if (ax == 2) {
     a.mean_out[row * 4 + 3] = 0.0f;
     if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
