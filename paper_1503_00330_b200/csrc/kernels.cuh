@@ -165,9 +165,10 @@ struct LwprArgs {
   int tile;             // fields per shared-memory tile when not resident
   int64_t rows;
   const float4 *x;      // (rows) inputs, padded to 4
-  float *mean_out;      // [row * out_stride + axis - a_begin]
+  float *mean_out;      // [row * row_stride + (axis - a_begin) * axis_stride]
   float *sd_out;        // std (sqrt_out) or variance; may be null
-  int out_stride;       // 4: float4 rows (xyz = axes, w = 0); 1: one axis
+  int row_stride;       // 1: planes (axis_stride = rows) or one axis; 4: float4 rows (w = 0)
+  int64_t axis_stride;
   int sqrt_out;
 };
 
@@ -459,12 +460,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
       } else {
         lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, xt[r], qr, gx, &mean, &var);
       }
-      const int64_t o = row * a.out_stride + (ax - a.a_begin);
+      const int64_t o = row * a.row_stride + (ax - a.a_begin) * a.axis_stride;
       a.mean_out[o] = mean;
       if (VAR && a.sd_out) a.sd_out[o] = a.sqrt_out ? __fsqrt_rn(var) : var;
       // float4 rows: the last pass also writes the pad lane, so every 32-byte
       // sector is fully written while it sits in L2 (no read-for-ownership)
-      if (a.out_stride == 4 && ax == a.a_end - 1) {
+      if (a.row_stride == 4 && ax == a.a_end - 1) {
         a.mean_out[row * 4 + 3] = 0.0f;
         if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
       }
@@ -489,11 +490,16 @@ struct RollArgs {
   float two_point;  // TwoPointModel magnitude
   DynParams dp;
   const float4 *xin, *ang_last;
-  const float4 *lw_mean, *lw_std;
+  const float *lw_mean, *lw_std;  // LWPR mean / std planes: axis c of row r at [c * lw_plane + r]
+  int64_t lw_plane;
   const float *dyn;  // (K, M, N, 3)
   double *costs;     // (K, N)
   uint8_t *crash;    // (K)
 };
+
+__device__ __forceinline__ float3 ld_planes(const float *p, int64_t plane, int64_t row) {
+  return make_float3(__ldg(p + row), __ldg(p + plane + row), __ldg(p + 2 * plane + row));
+}
 
 __device__ __forceinline__ float sign_of(float v) {  // np.sign (0 -> 0, NaN -> NaN)
   return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : v);
@@ -576,17 +582,18 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   // the analytic model's input row of step t + 1 is this step's post-step attitude row
   const bool hybrid = model == PI2_MODEL_HYBRID_LWPR;
   const bool with_std = hybrid && a.spread;
-  float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n;
-  if (hybrid) m4n = __ldg(a.lw_mean + k);
-  if (with_std) s4n = __ldg(a.lw_std + k);
+  float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
+  if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, k);
+  if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, k);
   float4 apn = (1 < N) ? __ldg(a.xin + a.K + k) : __ldg(a.ang_last + k);
-  float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldg(a.xin + k) : m4n;
+  float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
-    const float4 m4 = m4n, s4 = s4n, ap = apn;
+    const float3 m4 = m4n, s4 = s4n;
+    const float4 ap = apn;
     if (t + 1 < N) {
-      if (hybrid) m4n = __ldg(a.lw_mean + row + a.K);
-      if (with_std) s4n = __ldg(a.lw_std + row + a.K);
+      if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
+      if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
       apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + k);
     }
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
@@ -611,9 +618,9 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
     }
     float angterm = __fmul_rn(
         __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
-    // consume the finite pad lanes so ptxas keeps the in-flight prefetch registers (see
+    // consume the finite pad lane so ptxas keeps the in-flight prefetch registers (see
     // rollout_group_kernel)
-    angterm = fmaf(__fadd_rn(__fadd_rn(m4.w, s4.w), ap.w), 0.0f, angterm);
+    angterm = fmaf(ap.w, 0.0f, angterm);
     xr = ap;  // the analytic model's input row of step t + 1
     const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
     float q[MCAP];
@@ -738,21 +745,23 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   bool crashed = false;
   const bool hybrid = FAST || a.model == PI2_MODEL_HYBRID_LWPR;
   // rows of step t+1 are loaded while step t computes (hides HBM latency)
-  float4 m4n = make_float4(0.f, 0.f, 0.f, 0.f), s4n = m4n, apn = m4n;
+  float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
+  float4 apn = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active) {
     if (hybrid) {
-      m4n = __ldg(a.lw_mean + kk);
-      s4n = __ldg(a.lw_std + kk);
+      m4n = ld_planes(a.lw_mean, a.lw_plane, kk);
+      s4n = ld_planes(a.lw_std, a.lw_plane, kk);
     }
     apn = (1 < N) ? __ldg(a.xin + a.K + kk) : __ldg(a.ang_last + kk);
   }
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + kk;
-    const float4 m4 = m4n, s4 = s4n, ap = apn;
+    const float3 m4 = m4n, s4 = s4n;
+    const float4 ap = apn;
     if (active && t + 1 < N) {
       if (hybrid) {
-        m4n = __ldg(a.lw_mean + row + a.K);
-        s4n = __ldg(a.lw_std + row + a.K);
+        m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
+        s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
       }
       apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + kk);
     }
@@ -768,10 +777,10 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       }
       float angterm = __fmul_rn(
           __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
-      // consume the (finite) pad lanes of the prefetched rows: an unused .w lets ptxas
-      // reuse that register while the next step's 128-bit load is still in flight, a
-      // write-after-write stall of a full DRAM latency per step (ncu, rollout kernel)
-      angterm = fmaf(__fadd_rn(__fadd_rn(m4.w, s4.w), ap.w), 0.0f, angterm);
+      // consume the (finite) pad lane of the prefetched attitude row: an unused .w lets
+      // ptxas reuse that register while the next step's 128-bit load is still in flight,
+      // a write-after-write stall of a full DRAM latency per step (ncu, rollout kernel)
+      angterm = fmaf(ap.w, 0.0f, angterm);
       const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
       float d[3];
       if (device_dyn) {
@@ -931,7 +940,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
     const int64_t row = (int64_t)t * a.K + k;
     float mn[3];
     if (model == PI2_MODEL_HYBRID_LWPR) {
-      const float4 m4 = __ldg(a.lw_mean + row);
+      const float3 m4 = ld_planes(a.lw_mean, a.lw_plane, row);
       mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
     } else if (model == PI2_MODEL_ANALYTIC) {
       const float4 xr = __ldg(a.xin + row);

@@ -57,7 +57,8 @@ struct LwprTcArgs {
   const float *params;   // kLayShared records (exact path)
   int64_t rows;
   const float4 *x;
-  float *mean_out, *sd_out;  // float4 rows (xyz = axes, w = 0)
+  float *mean_out, *sd_out;  // planes: axis c of row r at [c * plane + r]
+  int64_t plane;
   int sqrt_out;
 };
 
@@ -249,12 +250,8 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
   } else {
     lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
   }
-  a.mean_out[row * 4 + ax] = mean;
-  if (VAR && a.sd_out) a.sd_out[row * 4 + ax] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
-  if (ax == 2) {
-    a.mean_out[row * 4 + 3] = 0.0f;
-    if (VAR && a.sd_out) a.sd_out[row * 4 + 3] = 0.0f;
-  }
+  a.mean_out[ax * a.plane + row] = mean;  // a warp writes 128 contiguous bytes
+  if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
 }
 
 // Per CTA the tiles are software-pipelined: while the tensor core computes the

@@ -60,7 +60,7 @@ struct pi2_ctx {
   uint8_t *d_io = nullptr;
   StepArgs *d_args = nullptr;
   double *d_plan = nullptr, *d_plan2 = nullptr;
-  float4 *d_xin = nullptr, *d_ang_last = nullptr, *d_lw = nullptr;  // d_lw: mean rows then std rows
+  float4 *d_xin = nullptr, *d_ang_last = nullptr, *d_lw = nullptr;  // d_lw: LWPR mean planes, std planes
   double *d_costs = nullptr;
   uint8_t *d_crash = nullptr;
   double *d_partials = nullptr, *d_root = nullptr;
@@ -211,6 +211,7 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   a.x = x;
   a.mean_out = mean_out;
   a.sd_out = sd_out;
+  a.plane = rows;
   a.sqrt_out = 1;
   auto *fn = lwpr_tc_kernel<VAR>;
   TRY(set_smem(ctx, fn, ctx->tc_smem));
@@ -223,12 +224,14 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   return PI2_OK;
 }
 
+// outputs: element (row, axis) at out[row * row_stride + (axis - a_begin) * axis_stride]
 int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
-                float *sd_out, int stride, int sqrt_out, cudaStream_t st) {
+                float *sd_out, int row_stride, int64_t axis_stride, int sqrt_out, cudaStream_t st) {
   TRY(ensure_params(ctx));
-  // all three axes into float4 rows (the rollout path): tensor cores when eligible
+  // all three axes into planes (the rollout path): tensor cores when eligible
   // (shared metric, each axis' weights fit at full residency; PI2_LWPR_TC=0 disables)
-  if (ctx->tc_ok && tc_wanted(ctx, sd_out != nullptr) && a_begin == 0 && a_end == 3 && stride == 4 && sqrt_out)
+  if (ctx->tc_ok && tc_wanted(ctx, sd_out != nullptr) && a_begin == 0 && a_end == 3 && row_stride == 1 &&
+      axis_stride == rows && sqrt_out)
     return sd_out ? launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st)
                   : launch_lwpr_tc<false>(ctx, rows, x, mean_out, nullptr, st);
   LwprArgs a{};
@@ -259,7 +262,8 @@ int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4
   a.x = x;
   a.mean_out = mean_out;
   a.sd_out = sd_out;
-  a.out_stride = stride;
+  a.row_stride = row_stride;
+  a.axis_stride = axis_stride;
   a.sqrt_out = sqrt_out;
   const bool var = sd_out != nullptr;
   const bool small = rows < (int64_t)2 * 148 * kLwprBlock * kLwprRows;
@@ -419,10 +423,10 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   CU(cudaGetLastError());
   if (ev) CU(cudaEventRecord(ev[1], st));
   const bool sp = spread(ctx);
-  float4 *lw_mean = ctx->d_lw, *lw_std = ctx->d_lw + K * N;
+  // LWPR outputs as planes: mean x|y|z then std x|y|z, K*N floats each
+  float *lw_mean = reinterpret_cast<float *>(ctx->d_lw), *lw_std = lw_mean + 3 * K * N;
   if (ctx->model == PI2_MODEL_HYBRID_LWPR)
-    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, reinterpret_cast<float *>(lw_mean),
-                    sp ? reinterpret_cast<float *>(lw_std) : nullptr, 4, 1, st));
+    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, lw_mean, sp ? lw_std : nullptr, 1, K * N, 1, st));
   if (ev) CU(cudaEventRecord(ev[2], st));
   RollArgs a{};
   a.sa = ctx->d_args;
@@ -440,6 +444,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   a.ang_last = ctx->d_ang_last;
   a.lw_mean = lw_mean;
   a.lw_std = lw_std;
+  a.lw_plane = K * N;
   a.dyn = dyn_dev;
   a.costs = costs;
   a.crash = crash;
@@ -1060,7 +1065,7 @@ int pi2_lwpr_predict(pi2_ctx *ctx, int32_t axis, int64_t rows, const float *X, f
   float4 *dx = (float4 *)ctx->d_scratch;
   float *dm = (float *)(dx + rows), *dv = dm + rows;
   CU(cudaMemcpyAsync(dx, xp.data(), xb, cudaMemcpyHostToDevice, st));
-  TRY(launch_lwpr(ctx, axis, axis + 1, rows, dx, dm, var_out ? dv : nullptr, 1, 0, st));
+  TRY(launch_lwpr(ctx, axis, axis + 1, rows, dx, dm, var_out ? dv : nullptr, 1, 0, 0, st));
   CU(cudaMemcpyAsync(mean_out, dm, ob, cudaMemcpyDeviceToHost, st));
   if (var_out) CU(cudaMemcpyAsync(var_out, dv, ob, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));

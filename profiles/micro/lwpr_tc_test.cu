@@ -53,7 +53,7 @@ int main(int argc, char **argv) {
   la.params = dparams;
   for (int i = 0; i < 3; ++i) la.axis[i] = hdr[i];
   la.a_begin = 0; la.a_end = 3; la.layout = kLayShared; la.resident = 1;
-  la.rows = rows; la.x = dx; la.mean_out = m1; la.sd_out = s1; la.out_stride = 4; la.sqrt_out = 1;
+  la.rows = rows; la.x = dx; la.mean_out = m1; la.sd_out = s1; la.row_stride = 1; la.axis_stride = rows; la.sqrt_out = 1;
   const int smem1 = (int)(rec.size() * 4);
   auto *k1 = lwpr_kernel<kLayShared, true, 8>;
   cudaFuncSetAttribute((const void *)k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
@@ -61,7 +61,7 @@ int main(int argc, char **argv) {
 
   ta.params = dparams;
   for (int i = 0; i < 3; ++i) ta.axis[i] = hdr[i];
-  ta.w = dblob; ta.rows = rows; ta.x = dx; ta.mean_out = m2; ta.sd_out = s2; ta.sqrt_out = 1;
+  ta.w = dblob; ta.rows = rows; ta.x = dx; ta.mean_out = m2; ta.sd_out = s2; ta.plane = rows; ta.sqrt_out = 1;
   int64_t wmax = 0;
   for (int i = 0; i < 3; ++i) {
     const int64_t we = i < 2 ? ta.axis_off[i + 1] : ta.w_floats;
@@ -106,7 +106,6 @@ int main(int argc, char **argv) {
   double dm = 0, ds = 0, mm = 0;
   int64_t bad = 0;
   for (int64_t i = 0; i < rows * 4; ++i) {
-    if (i % 4 == 3) continue;
     const double d1 = fabs(a1[i] - a2[i]), d2 = fabs(b1[i] - b2[i]) / fmax(1e-6, fabs(b1[i]));
     if (!(d1 <= 1e30)) ++bad;
     dm = fmax(dm, d1); ds = fmax(ds, d2); mm = fmax(mm, fabs(a1[i]));
