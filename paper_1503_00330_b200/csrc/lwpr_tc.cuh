@@ -42,7 +42,8 @@ namespace pi2 {
 constexpr int kTcChunk = PI2_TC_CHUNK;        // max fields per MMA chunk (N = 2 * kTcChunk TMEM columns)
 constexpr int kTcTmemCols = 2 * PI2_TC_CHUNK;  // power of two >= 32
 
-constexpr int kTcMaxChunks = 16;    // fields per axis <= 16 * kTcChunk on this path
+constexpr int kTcMaxChunks = 32;    // fields per axis <= 32 * kTcChunk on this path
+constexpr int kTcWSlotFloats = 2 * 2 * kTcChunk * 8;  // W of one chunk (hi + lo), streamed mode slot
 
 struct LwprTcArgs {
   const float *w;        // per axis, per chunk: W_hi then W_lo, each (2*Lc_pad rows x 8) in UMMA layout,
@@ -52,7 +53,8 @@ struct LwprTcArgs {
   int64_t axis_off[3];   // float offset of each axis' first chunk in w
   int64_t lv_off[3];     // float offset of each axis' variances (after the W matrices)
   int nchunks[3];
-  int chunk_pad[3][kTcMaxChunks];  // padded field count of each chunk (multiple of 16), <= kTcChunk
+  int chunk_pad[3][kTcMaxChunks];  // padded field count of each chunk (multiple of 8), <= kTcChunk
+  int chunk_woff[3][kTcMaxChunks]; // float offset of each chunk's W within its axis' block
   AxisHeader axis[3];    // headers of the kLayShared records (exact path, g, mu, qd)
   const float *params;   // kLayShared records (exact path)
   int64_t rows;
@@ -258,24 +260,44 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
 // first chunk of tile t, the CUDA cores finalize tile t - 1 and write tile t + 1's
 // features into the other A buffer (its x was loaded one tile ahead), so only the
 // barrier, the MMA latency and the exp phase remain on the critical path.
-template <bool VAR>
+// STREAM: the axis' W does not fit in shared memory next to 3 other CTAs (large L):
+// each chunk's W (<= 8 KB, L2-resident, read by every CTA of the axis) is brought in
+// by a TMA bulk copy into a 2-slot ring, one chunk ahead of its MMA.
+template <bool VAR, bool STREAM>
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprTcArgs a) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t wbar[2];  // STREAM: W slot s holds its chunk
   // CTA i evaluates axis i % 3 for tiles i / 3, i / 3 + gridDim.x / 3, ...: only that
   // axis' weights (W chunks, then its chunk-padded variances) live in shared memory
   const int ax = blockIdx.x % 3;
+  const int nch = a.nchunks[ax];
   const int64_t wbeg = a.axis_off[ax], wend = ax < 2 ? a.axis_off[ax + 1] : a.w_floats;
-  const int64_t nlv = (int64_t)a.nchunks[ax] * kTcChunk;
+  const int64_t nlv = (int64_t)nch * kTcChunk;
+  const int64_t wfl = STREAM ? 2 * kTcWSlotFloats : wend - wbeg;  // resident W, or the 2-slot ring
   float *sw = reinterpret_cast<float *>(tsm);
-  float *slv_base = sw + (wend - wbeg);
-  uint8_t *sa = tsm + (((wend - wbeg + nlv) * 4 + 127) / 128) * 128;  // two A operands
+  float *slv_base = sw + wfl;
+  uint8_t *sa = tsm + (((wfl + nlv) * 4 + 127) / 128) * 128;  // two A operands
   const int tid = threadIdx.x, warp = tid >> 5;
 
-  for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
-    reinterpret_cast<float4 *>(sw)[i] = __ldg(reinterpret_cast<const float4 *>(a.w + wbeg) + i);
+  if (!STREAM)
+    for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
+      reinterpret_cast<float4 *>(sw)[i] = __ldg(reinterpret_cast<const float4 *>(a.w + wbeg) + i);
   for (int64_t i = tid; i < nlv; i += blockDim.x) slv_base[i] = __ldg(a.w + a.lv_off[ax] + i);
+  const uint32_t wbar_addr = (uint32_t)__cvta_generic_to_shared(&wbar[0]);
+  const uint32_t sw_addr0 = (uint32_t)__cvta_generic_to_shared(sw);
+  // bulk-copy chunk c's W into slot `slot` (thread 0)
+  auto load_w = [&](int c, uint32_t slot) {
+    const uint32_t bytes = (uint32_t)(2 * 2 * a.chunk_pad[ax][c] * 8 * 4);
+    const uint32_t bar = wbar_addr + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            sw_addr0 + slot * (uint32_t)(kTcWSlotFloats * 4)),
+        "l"(a.w + wbeg + a.chunk_woff[ax][c]), "r"(bytes), "r"(bar)
+        : "memory");
+  };
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tmem_base)),
@@ -285,7 +307,12 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   const uint32_t mbar_addr = (uint32_t)__cvta_generic_to_shared(&mbar);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_addr));
+    if (STREAM) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr + 8));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
+    if (STREAM && blockIdx.x / 3 < (a.rows + 127) / 128) load_w(0, 0);
   }
   const AxisHeader &h = a.axis[ax];
   const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
@@ -308,7 +335,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   const uint32_t tmem = tmem_base;
   const uint32_t tmem_lane = tmem + ((uint32_t)(warp * 32) << 16);
   const uint32_t sw_addr = (uint32_t)__cvta_generic_to_shared(sw);
-  uint32_t phase = 0;
+  uint32_t phase = 0, nw = 0;  // nw: chunks issued by this CTA (W ring position)
   int buf = 0;
 #ifdef PI2_TC_PROF
   long long prof[5] = {0, 0, 0, 0, 0}, t_last = clock64();
@@ -320,7 +347,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
     float4 xt_next = xt;
     float q_next = q;
     int64_t woff = 0;  // within this axis' block in shared memory
-    for (int c = 0; c < a.nchunks[ax]; ++c) {
+    for (int c = 0; c < nch; ++c, ++nw) {
       const int lc = a.chunk_pad[ax][c];  // fields of this chunk, multiple of 8, 2 lc <= 128 columns
       asm volatile("fence.proxy.async.shared::cta;");
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -330,13 +357,16 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
         const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
-        const uint32_t wb = sw_addr + (uint32_t)(woff * 4);
+        if (STREAM) mbar_wait(wbar_addr + 8 * (nw & 1), (nw >> 1) & 1);  // this chunk's W landed
+        const uint32_t wb = STREAM ? sw_addr + (nw & 1) * (uint32_t)(kTcWSlotFloats * 4) : sw_addr + (uint32_t)(woff * 4);
         const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
         mma_tf32(tmem, a_hi, b_hi, idesc, 0);
         mma_tf32(tmem, a_hi, b_lo, idesc, 1);
         mma_tf32(tmem, a_lo, b_hi, idesc, 1);
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             mbar_addr));
+        // the other slot held chunk nw - 1, whose MMA completed before this chunk's barrier
+        if (STREAM && (c + 1 < nch || tile + tstride < ntiles)) load_w(c + 1 < nch ? c + 1 : 0, (nw + 1) & 1);
       }
       if (c == 0) {  // in the MMA's shadow: finish tile t - 1, stage tile t + 1
         tc_finalize<VAR>(a, h, ax, row_prev, xt_prev, q_prev, dn_p, nm_p, m2_p, lv_p);
@@ -453,6 +483,7 @@ inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, Lwpr
       const int l0 = c * per, n = std::min(per, a.L - l0);
       const int lc = (n + 7) / 8 * 8;
       ta.chunk_pad[ax][c] = lc;
+      ta.chunk_woff[ax][c] = (int)(w_floats - ta.axis_off[ax]);
       std::vector<float> hi(2 * lc * 8, 0.0f), lo(2 * lc * 8, 0.0f);
       auto put = [&](int r, int k, double v) {
         const float f = (float)v, fh = host_tf32_rna(f);

@@ -50,6 +50,7 @@ struct pi2_ctx {
   bool tc_ok = false;
   bool tc_enabled = true;  // PI2_LWPR_TC=0 forces the CUDA-core kernel
   int tc_mode = 1;         // see tc_wanted
+  bool tc_stream = false;  // W streamed per chunk (large L)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -164,12 +165,19 @@ int ensure_params(pi2_ctx *ctx) {
       TRY(ensure(ctx, (void **)&ctx->d_tc, &ctx->tc_cap, blob.size() * sizeof(float)));
       CU(cudaMemcpy(ctx->d_tc, blob.data(), blob.size() * sizeof(float), cudaMemcpyHostToDevice));
       ta.w = ctx->d_tc;
-      int64_t wmax = 0;
+      int64_t wmax = 0, lvmax = 0;
       for (int i = 0; i < 3; ++i) {
         const int64_t we = i < 2 ? ta.axis_off[i + 1] : ta.w_floats;
         wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
+        lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
       }
-      ctx->tc_smem = tc_smem_bytes(wmax, (const void *)lwpr_tc_kernel<true>);
+      // W resident in shared memory when it fits next to 3 other CTAs, else streamed
+      ctx->tc_stream = false;
+      ctx->tc_smem = tc_smem_bytes(wmax, (const void *)lwpr_tc_kernel<true, false>);
+      if (ctx->tc_smem < 0 || getenv("PI2_LWPR_TC_STREAM")) {
+        ctx->tc_stream = true;
+        ctx->tc_smem = tc_smem_bytes(2 * kTcWSlotFloats + lvmax, (const void *)lwpr_tc_kernel<true, true>);
+      }
       ctx->tc = ta;
       ctx->tc_ok = ctx->tc_smem > 0 && ctx->tc_smem <= ctx->smem_optin;
     }
@@ -213,7 +221,7 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   a.sd_out = sd_out;
   a.plane = rows;
   a.sqrt_out = 1;
-  auto *fn = lwpr_tc_kernel<VAR>;
+  auto *fn = ctx->tc_stream ? lwpr_tc_kernel<VAR, true> : lwpr_tc_kernel<VAR, false>;
   TRY(set_smem(ctx, fn, ctx->tc_smem));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);

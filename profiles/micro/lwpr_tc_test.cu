@@ -68,9 +68,19 @@ int main(int argc, char **argv) {
     wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
   }
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
-  auto *k2 = lwpr_tc_kernel<true>;
-  const int smem2 = tc_smem_bytes(wmax, (const void *)k2);
-  if (smem2 < 0) { printf("W does not fit %d CTAs/SM\n", kTcCtasPerSm); return 1; }
+  int64_t lvmax = 0;
+  for (int i = 0; i < 3; ++i) lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
+  auto *k2 = lwpr_tc_kernel<true, false>;
+  auto *k4 = lwpr_tc_kernel<false, false>;
+  int smem2 = tc_smem_bytes(wmax, (const void *)k2);
+  const bool stream = smem2 < 0 || getenv("STREAM");
+  if (stream) {  // W streamed per chunk
+    k2 = lwpr_tc_kernel<true, true>;
+    k4 = lwpr_tc_kernel<false, true>;
+    smem2 = tc_smem_bytes(2 * kTcWSlotFloats + lvmax, (const void *)k2);
+  }
+  printf("W %s\n", stream ? "streamed" : "resident");
+  if (smem2 < 0) { printf("does not fit %d CTAs/SM\n", kTcCtasPerSm); return 1; }
   cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned g2 = (kTcCtasPerSm * sms) / 3 * 3;
@@ -118,7 +128,6 @@ int main(int argc, char **argv) {
   {  // mean only (M = 1 rollouts)
     auto *k3 = lwpr_kernel<kLayShared, false, 8>;
     cudaFuncSetAttribute((const void *)k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
-    auto *k4 = lwpr_tc_kernel<false>;
     cudaFuncSetAttribute((const void *)k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     la.sd_out = nullptr;
     ta.sd_out = nullptr;

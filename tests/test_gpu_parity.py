@@ -437,6 +437,34 @@ def test_tiled_parameters_match_oracle(L, full):
     assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
 
 
+@pytest.mark.parametrize("L,M,tc", [(1000, 1, "1"), (600, 2, "1"), (1000, 2, "0")])
+def test_large_shared_metric_models_match_oracle(L, M, tc, monkeypatch):
+    """Shared-metric models too large for resident weights (C3): the tensor-core kernel
+    streams each chunk's weights (PI2_LWPR_TC=1), the CUDA-core kernel tiles them (0)."""
+    monkeypatch.setenv("PI2_LWPR_TC", tc)
+    stacks = synthetic.hybrid_stacks(L, seed=L + M)
+    K, N = 20000, 6
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=5)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn)
+    plan = P.ControlPlan.hover(params, N)
+    noise = P.sample_noise(cfg, 0, 0)
+    dyn = P.sample_dynamics_noise(cfg, 0, 0) if M > 1 else None
+    eng = P.RolloutEngine(model, cfg, device=0)
+    b = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn)
+    kind = _abi.C.c_int32()
+    eng.context(K, N).call("pi2_lwpr_kernel", int(M > 1), _abi.C.byref(kind), None)
+    assert kind.value == (1 if tc == "1" else 0)
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise,
+                         RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES), dyn, M)
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
 def test_shared_metric_model_from_reference_training():
     """A model trained by the reference (fields share d_init) through the LWPR1 format."""
     z = load("persistence")
