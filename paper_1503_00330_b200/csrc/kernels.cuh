@@ -16,6 +16,20 @@
 
 namespace pi2 {
 
+// Programmatic dependent launch: the step's kernels are launched with
+// programmatic stream serialization, so a kernel may start while its predecessor
+// drains.  pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible (a no-op for a normal launch): every kernel calls it before
+// touching anything an earlier kernel of the step writes; only constants
+// (StepArgs, model weights) and TMEM allocation come before it.  Data written by
+// the IMMEDIATE predecessor is read with coherent loads (__ldcg): a non-coherent
+// __ldg (ld.global.nc) promises read-only data for the whole kernel, and ptxas
+// does hoist it above griddepcontrol.wait (seen in SASS: a race).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel of the step launch (its CTAs then spin in pdl_wait)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+
 // ---------------------------------------------------------------------------
 // device noise: Philox4x32-10 + Box-Muller, keyed by the reference's stream
 // address (rng.py:33-44); counter = element-group index + key word 1.
@@ -101,6 +115,8 @@ __global__ void __launch_bounds__(kRolloutBlock)
                     DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last,
                     double *__restrict__ eps_out) {
   extern __shared__ double splan[];  // (N, 4)
+  pdl_wait();     // the plan is the previous iteration's update
+  pdl_trigger();  // one wave: the LWPR kernel's prologue may start on free SM resources
   for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) splan[i] = plan[i];
   __syncthreads();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -371,13 +387,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
   constexpr int P = R / 2;
   extern __shared__ float4 smem4[];
   float *srec = reinterpret_cast<float *>(smem4);
+  pdl_wait();
 
   const int64_t row0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R;
   float4 x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t row = row0 + r < a.rows ? row0 + r : a.rows - 1;
-    x[r] = __ldg(a.x + row);
+    x[r] = __ldcg(a.x + row);  // the attitude kernel's output (see pdl_wait)
   }
   float2 X[P][4];
 #pragma unroll
@@ -497,8 +514,9 @@ struct RollArgs {
   uint8_t *crash;    // (K)
 };
 
+// the LWPR kernel's output: coherent loads (see pdl_wait)
 __device__ __forceinline__ float3 ld_planes(const float *p, int64_t plane, int64_t row) {
-  return make_float3(__ldg(p + row), __ldg(p + plane + row), __ldg(p + 2 * plane + row));
+  return make_float3(__ldcg(p + row), __ldcg(p + plane + row), __ldcg(p + 2 * plane + row));
 }
 
 __device__ __forceinline__ float sign_of(float v) {  // np.sign (0 -> 0, NaN -> NaN)
@@ -554,6 +572,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   __shared__ pi2_cost cost;
   if (threadIdx.x == 0) cost = a.sa->cost;
   __syncthreads();
+  pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= a.K) return;
   const int M = MM > 0 ? MM : a.M;
@@ -721,6 +740,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   __shared__ pi2_cost cost;
   if (threadIdx.x == 0) cost = a.sa->cost;
   __syncthreads();
+  pdl_wait();
   const int lane_g = threadIdx.x % G, grp = threadIdx.x / G;
   const int64_t k = (int64_t)blockIdx.x * RPB + grp;
   const bool live = k < a.K;
@@ -887,6 +907,8 @@ __global__ void __launch_bounds__(32 * kWideWarps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *u = splan + 4 * N + (size_t)warp * 4 * N;      // (N, 4) clipped controls of this rollout
   float4 *stage = reinterpret_cast<float4 *>(splan + 4 * N + (size_t)kWideWarps * 4 * N) + (size_t)warp * (N + 1);
+  pdl_wait();
+  pdl_trigger();
   for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) splan[i] = plan[i];
   __syncthreads();
   const int64_t k = (int64_t)blockIdx.x * kWideWarps + warp;
@@ -926,6 +948,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
   __shared__ pi2_cost cost;
   if (threadIdx.x == 0) cost = a.sa->cost;
   __syncthreads();
+  pdl_wait();
   const int N = a.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per warp: acc (N,3) -> cs (N,3), ccs (N,3), angterm (N), q (N)
@@ -1041,6 +1064,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
                     const double *__restrict__ eps, const StepArgs *__restrict__ sa, int iteration,
                     int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
   constexpr int J = kChunk / 32;
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.y * kChunkWarps + warp;  // one warp per (chunk, t)
   if (t >= N) return;
@@ -1050,7 +1074,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int64_t k = k0 + lane + 32 * j;
-    s[j] = k < K ? __ldg(costs + k * cs_k + t * cs_t) : INFINITY;  // S(k, t)
+    s[j] = k < K ? __ldcg(costs + k * cs_k + t * cs_t) : INFINITY;  // S(k, t); coherent (see pdl_wait)
     m = fmin(m, s[j]);
   }
   m = warp_min(m);
@@ -1103,11 +1127,12 @@ __global__ void transpose_costs_kernel(const double *__restrict__ src, double *_
 // plan[t] += V/Z of a single partial, clipped (the world-size-1 finalize)
 __global__ void apply_root_kernel(const double *__restrict__ root, int N, double *__restrict__ plan,
                                   DynParams dp) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 4 * N) return;
   const int t = i / 4, c = i % 4;
   const double *r = root + t * PI2_PARTIAL_WIDTH;
-  const double du = __ddiv_rn(r[2 + c], r[1]);
+  const double du = __ddiv_rn(__ldcg(r + 2 + c), __ldcg(r + 1));  // coherent (see pdl_wait)
   plan[i] = clip_np(__dadd_rn(plan[i], du), dp.lo[c], dp.hi[c]);
 }
 
@@ -1135,6 +1160,7 @@ __global__ void __launch_bounds__(256)
   extern __shared__ double cmb[];
   double(*seg)[PI2_PARTIAL_WIDTH] = reinterpret_cast<double(*)[PI2_PARTIAL_WIDTH]>(cmb);
   double(*roots)[PI2_PARTIAL_WIDTH] = seg + kSeg;
+  pdl_wait();
   const int t = blockIdx.x;
   const int64_t nseg = (n + kSeg - 1) / kSeg;
   for (int64_t s = 0; s < nseg; ++s) {
@@ -1142,7 +1168,7 @@ __global__ void __launch_bounds__(256)
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
       const double *src = leaves + ((s * kSeg + i) * N + t) * PI2_PARTIAL_WIDTH;
 #pragma unroll
-      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) seg[i][c] = src[c];
+      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) seg[i][c] = __ldcg(src + c);  // coherent (see pdl_wait)
     }
     __syncthreads();
     smem_tree(seg, cnt, neg_inv);

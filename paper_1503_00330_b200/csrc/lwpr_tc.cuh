@@ -318,15 +318,19 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
   const int64_t tstride = gridDim.x / 3;
   int64_t tile = blockIdx.x / 3;
+  // the rows are the attitude kernel's output (weights, TMEM and barriers above are
+  // not): wait for it, then read them with coherent loads (__ldcg) -- ptxas may
+  // hoist a non-coherent __ldg above griddepcontrol.wait
+  pdl_wait();
   float4 xt, xt_prev = make_float4(0.f, 0.f, 0.f, 0.f);
   float q, q_prev = 0.0f, dn_p = 0.0f, nm_p = 0.0f, m2_p = 0.0f, lv_p = 0.0f;
   int64_t row_prev = a.rows;  // nothing to finalize yet
   {
     const int64_t r0 = tile * 128 + tid;
-    tc_features(h, __ldg(a.x + (r0 < last ? r0 : last)), sa, tid, xt, q);
+    tc_features(h, __ldcg(a.x + (r0 < last ? r0 : last)), sa, tid, xt, q);
   }
   int64_t rn = (tile + tstride) * 128 + tid;
-  float4 xn = __ldg(a.x + (rn < last ? rn : last));  // next tile's inputs, one tile ahead
+  float4 xn = __ldcg(a.x + (rn < last ? rn : last));  // next tile's inputs, one tile ahead
 
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
         if (tile + tstride < ntiles) {
           tc_features(h, xn, sa + (buf ^ 1) * kTcABytes, tid, xt_next, q_next);
           rn = (tile + 2 * tstride) * 128 + tid;
-          xn = __ldg(a.x + (rn < last ? rn : last));
+          xn = __ldcg(a.x + (rn < last ? rn : last));
         }
         PI2_TC_T(0);
       }

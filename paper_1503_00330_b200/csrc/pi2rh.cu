@@ -51,6 +51,7 @@ struct pi2_ctx {
   bool tc_enabled = true;  // PI2_LWPR_TC=0 forces the CUDA-core kernel
   int tc_mode = 1;         // see tc_wanted
   bool tc_stream = false;  // W streamed per chunk (large L)
+  bool pdl = true;         // programmatic dependent launch along the step's kernels (PI2_PDL=0: off)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -193,15 +194,41 @@ int set_smem(pi2_ctx *ctx, F *fn, int bytes) {
   return PI2_OK;
 }
 
+// a kernel of the step's chain, launched with programmatic stream serialization
+// (PDL, see pdl_wait in kernels.cuh) unless PI2_PDL=0 or `pdl` is false.  Only
+// for kernels whose stream predecessor is a kernel of the chain: griddepcontrol.wait
+// waits for the previous GRID, not for a copy or an event wait before it.
+template <typename... KArgs, typename... Args>
+int launch_pdl_if(bool pdl, pi2_ctx *ctx, void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                  Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = (pdl && ctx->pdl) ? 1 : 0;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...));
+  return PI2_OK;
+}
+template <typename... KArgs, typename... Args>
+int launch_pdl(pi2_ctx *ctx, void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args &&...args) {
+  return launch_pdl_if(true, ctx, fn, grid, block, smem, st, std::forward<Args>(args)...);
+}
+
 int lwpr_smem_limit(pi2_ctx *ctx) { return std::min(ctx->smem_optin, 64 * 1024); }
 
 template <int LAY, bool VAR, int R>
-int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st) {
+int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st, bool pdl) {
   auto *fn = lwpr_kernel<LAY, VAR, R>;
   TRY(set_smem(ctx, fn, smem));
   const int64_t per_block = (int64_t)kLwprBlock * R;
   const int64_t grid = (a.rows + per_block - 1) / per_block;
-  fn<<<(unsigned)grid, kLwprBlock, smem, st>>>(a);
+  TRY(launch_pdl_if(pdl, ctx, fn, dim3((unsigned)grid), dim3(kLwprBlock), smem, st, a));
   CU(cudaGetLastError());
   return PI2_OK;
 }
@@ -211,7 +238,8 @@ int launch_lwpr_t(pi2_ctx *ctx, LwprArgs a, int smem, cudaStream_t st) {
 bool tc_wanted(const pi2_ctx *ctx, bool var) { return ctx->tc_mode == 1 || (ctx->tc_mode == 2 && var); }
 
 template <bool VAR>
-int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out, float *sd_out, cudaStream_t st) {
+int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out, float *sd_out, cudaStream_t st,
+                   bool pdl) {
   LwprTcArgs a = ctx->tc;
   for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
   a.params = ctx->d_params;
@@ -227,21 +255,22 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const int64_t tiles = (rows + 127) / 128;
   const int64_t grid = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles) * 3;  // CTA i -> axis i % 3
-  fn<<<(unsigned)grid, kTcThreads, ctx->tc_smem, st>>>(a);
+  TRY(launch_pdl_if(pdl, ctx, fn, dim3((unsigned)grid), dim3(kTcThreads), ctx->tc_smem, st, a));
   CU(cudaGetLastError());
   return PI2_OK;
 }
 
 // outputs: element (row, axis) at out[row * row_stride + (axis - a_begin) * axis_stride]
+// pdl: the stream predecessor is the attitude kernel (rollout chain)
 int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
-                float *sd_out, int row_stride, int64_t axis_stride, int sqrt_out, cudaStream_t st) {
+                float *sd_out, int row_stride, int64_t axis_stride, int sqrt_out, cudaStream_t st, bool pdl = false) {
   TRY(ensure_params(ctx));
   // all three axes into planes (the rollout path): tensor cores when eligible
   // (shared metric, each axis' weights fit at full residency; PI2_LWPR_TC=0 disables)
   if (ctx->tc_ok && tc_wanted(ctx, sd_out != nullptr) && a_begin == 0 && a_end == 3 && row_stride == 1 &&
       axis_stride == rows && sqrt_out)
-    return sd_out ? launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st)
-                  : launch_lwpr_tc<false>(ctx, rows, x, mean_out, nullptr, st);
+    return sd_out ? launch_lwpr_tc<true>(ctx, rows, x, mean_out, sd_out, st, pdl)
+                  : launch_lwpr_tc<false>(ctx, rows, x, mean_out, nullptr, st, pdl);
   LwprArgs a{};
   a.params = ctx->d_params;
   for (int i = 0; i < 3; ++i) a.axis[i] = ctx->hdr[i];
@@ -277,10 +306,10 @@ int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4
   const bool small = rows < (int64_t)2 * 148 * kLwprBlock * kLwprRows;
 #define PI2_LWPR_CASE(LAY)                                                                          \
   if (ctx->layout == LAY) {                                                                         \
-    if (var) return small ? launch_lwpr_t<LAY, true, 2>(ctx, a, smem, st)                           \
-                          : launch_lwpr_t<LAY, true, kLwprRows>(ctx, a, smem, st);                  \
-    return small ? launch_lwpr_t<LAY, false, 2>(ctx, a, smem, st)                                   \
-                 : launch_lwpr_t<LAY, false, kLwprRows>(ctx, a, smem, st);                          \
+    if (var) return small ? launch_lwpr_t<LAY, true, 2>(ctx, a, smem, st, pdl)                           \
+                          : launch_lwpr_t<LAY, true, kLwprRows>(ctx, a, smem, st, pdl);                  \
+    return small ? launch_lwpr_t<LAY, false, 2>(ctx, a, smem, st, pdl)                                   \
+                 : launch_lwpr_t<LAY, false, kLwprRows>(ctx, a, smem, st, pdl);                          \
   }
   PI2_LWPR_CASE(kLayShared)
   PI2_LWPR_CASE(kLayDiag)
@@ -300,7 +329,7 @@ int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int smem = a.N * kRolloutBlock * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + kRolloutBlock - 1) / kRolloutBlock;
-  fn<<<(unsigned)grid, kRolloutBlock, smem, st>>>(a);
+  TRY(launch_pdl(ctx, fn, dim3((unsigned)grid), dim3(kRolloutBlock), smem, st, a));
   CU(cudaGetLastError());
   return PI2_OK;
 }
@@ -312,7 +341,7 @@ int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int smem = a.N * RPB * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + RPB - 1) / RPB;
-  fn<<<(unsigned)grid, kRolloutBlock, smem, st>>>(a);
+  TRY(launch_pdl(ctx, fn, dim3((unsigned)grid), dim3(kRolloutBlock), smem, st, a));
   CU(cudaGetLastError());
   return PI2_OK;
 }
@@ -340,10 +369,10 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     const int smem = kWideWarps * 11 * a.N * (int)sizeof(float);
     if (hybrid && nav) {
       TRY(set_smem(ctx, rollout_wide_kernel<true>, smem));
-      rollout_wide_kernel<true><<<grid, 32 * kWideWarps, smem, st>>>(a);
+      TRY(launch_pdl(ctx, rollout_wide_kernel<true>, dim3(grid), dim3(32 * kWideWarps), smem, st, a));
     } else {
       TRY(set_smem(ctx, rollout_wide_kernel<false>, smem));
-      rollout_wide_kernel<false><<<grid, 32 * kWideWarps, smem, st>>>(a);
+      TRY(launch_pdl(ctx, rollout_wide_kernel<false>, dim3(grid), dim3(32 * kWideWarps), smem, st, a));
     }
     CU(cudaGetLastError());
     return PI2_OK;
@@ -408,25 +437,24 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
     const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
     if (noise_dev) {
       TRY(set_smem(ctx, attitude_wide_kernel<false>, wsmem));
-      attitude_wide_kernel<false><<<wgrid, 32 * kWideWarps, wsmem, st>>>(
-          ctx->d_args, ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
-          ctx->d_ang_last);
+      TRY(launch_pdl_if(false, ctx, attitude_wide_kernel<false>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
+                     ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
+                     ctx->d_ang_last));
     } else {
       TRY(set_smem(ctx, attitude_wide_kernel<true>, wsmem));
-      attitude_wide_kernel<true><<<wgrid, 32 * kWideWarps, wsmem, st>>>(
-          ctx->d_args, ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
-          ctx->d_ang_last);
+      TRY(launch_pdl_if(false, ctx, attitude_wide_kernel<true>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
+                     ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
+                     ctx->d_ang_last));
     }
   } else if (noise_dev) {
     TRY(set_smem(ctx, attitude_kernel<false>, psmem));
-    attitude_kernel<false><<<grid, kRolloutBlock, psmem, st>>>(
-        ctx->d_args, ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp,
-        ctx->d_xin, ctx->d_ang_last, nullptr);
+    TRY(launch_pdl_if(false, ctx, attitude_kernel<false>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+                   noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last,
+                   nullptr));
   } else {
     TRY(set_smem(ctx, attitude_kernel<true>, psmem));
-    attitude_kernel<true><<<grid, kRolloutBlock, psmem, st>>>(
-        ctx->d_args, ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp,
-        ctx->d_xin, ctx->d_ang_last, nullptr);
+    TRY(launch_pdl_if(false, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+                   nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, nullptr));
   }
   CU(cudaGetLastError());
   if (ev) CU(cudaEventRecord(ev[1], st));
@@ -434,7 +462,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   // LWPR outputs as planes: mean x|y|z then std x|y|z, K*N floats each
   float *lw_mean = reinterpret_cast<float *>(ctx->d_lw), *lw_std = lw_mean + 3 * K * N;
   if (ctx->model == PI2_MODEL_HYBRID_LWPR)
-    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, lw_mean, sp ? lw_std : nullptr, 1, K * N, 1, st));
+    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, lw_mean, sp ? lw_std : nullptr, 1, K * N, 1, st, true));
   if (ev) CU(cudaEventRecord(ev[2], st));
   RollArgs a{};
   a.sa = ctx->d_args;
@@ -463,17 +491,18 @@ dim3 partials_grid(int64_t chunks, int N) {
   return dim3((unsigned)chunks, (unsigned)((N + kChunkWarps - 1) / kChunkWarps));
 }
 
+// after_kernel: the stream predecessor is the partials kernel (PDL allowed)
 int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
-                   double *plan, cudaStream_t st) {
+                   double *plan, cudaStream_t st, bool after_kernel = false) {
   if (n == 1 && !root && plan) {  // a single partial: just apply it
-    apply_root_kernel<<<(4 * N + 127) / 128, 128, 0, st>>>(leaves, N, plan, ctx->dp);
+    TRY(launch_pdl_if(after_kernel, ctx, apply_root_kernel, dim3((4 * N + 127) / 128), dim3(128), 0, st, leaves, N, plan, ctx->dp));
     CU(cudaGetLastError());
     return PI2_OK;
   }
   if ((n + kSeg - 1) / kSeg > kSeg) return fail(ctx, PI2_ERR_INVALID, "too many partials (%lld)", (long long)n);
   const int smem = 2 * kSeg * PI2_PARTIAL_WIDTH * (int)sizeof(double);
   TRY(set_smem(ctx, combine_kernel, smem));
-  combine_kernel<<<N, 256, smem, st>>>(leaves, n, N, neg_inv, root, plan, ctx->dp);
+  TRY(launch_pdl_if(after_kernel, ctx, combine_kernel, dim3(N), dim3(256), smem, st, leaves, n, N, neg_inv, root, plan, ctx->dp));
   CU(cudaGetLastError());
   return PI2_OK;
 }
@@ -482,12 +511,12 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
                      cudaStream_t st) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
-  partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
-      ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
-      ctx->d_partials);
+  TRY(launch_pdl(ctx, partials_kernel, partials_grid(ctx->n_chunks, ctx->N), dim3(32 * kChunkWarps), 0, st,
+                 ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N,
+                 neg_inv, ctx->d_partials));
   CU(cudaGetLastError());
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
-                        update_plan ? ctx->d_plan : nullptr, st);
+                        update_plan ? ctx->d_plan : nullptr, st, true);
 }
 
 int validate_opt(pi2_ctx *ctx, const pi2_optimize_args *args) {
@@ -570,6 +599,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   };
   if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (const char *e = getenv("PI2_PDL")) ctx->pdl = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_LWPR_TC")) {
     ctx->tc_mode = std::atoi(e);
     ctx->tc_enabled = ctx->tc_mode != 0;

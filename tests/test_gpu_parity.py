@@ -370,6 +370,35 @@ def test_receding_fast_path_equals_optimize_then_shift():
     assert ctrl.thrust == plan.controls[0, 3]
 
 
+@pytest.mark.parametrize("K,M", [(128, 2), (20000, 1), (3000, 4)])
+def test_programmatic_dependent_launch_is_bitwise_neutral(K, M, monkeypatch):
+    """The step's kernels overlap their predecessors' tails under PDL (PI2_PDL, default
+    on): results must be bitwise those of plain stream ordering, over repeated host-noise
+    evaluations (different contexts, copies before the chain) and device optimizations.
+    A non-coherent load hoisted above griddepcontrol.wait showed up exactly here."""
+    stacks = synthetic.hybrid_stacks(24, seed=K + M)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    task = P.Task.default()
+    plan = P.ControlPlan.hover(params, 20)
+    state = P.QuadState.hover(task.spawn)
+    res = {}
+    for pdl in ("1", "0"):
+        monkeypatch.setenv("PI2_PDL", pdl)
+        cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=20, iterations_per_step=2, rng_seed=1)
+        eng = P.RolloutEngine(model, cfg, device=0)
+        dev = P.RolloutEngine(model, cfg, device=0, noise="device")
+        out = []
+        for cyc in range(4):
+            noise = P.sample_noise(cfg, cyc, 0)
+            dyn = P.sample_dynamics_noise(cfg, cyc, 0) if M > 1 else None
+            out.append(eng.evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn).costs_to_go)
+            out.append(dev.optimize_device(state, plan, P.RolloutCost(task, 1), cyc).controls)
+        res[pdl] = out
+    for a, b in zip(res["1"], res["0"]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_sharded_partials_are_gpu_count_invariant():
     """Rank shards evaluated one after another on one GPU (no cross-waiting kernels):
     the fixed-order combine gives the single-context plan bitwise for G = 2 and 4."""
