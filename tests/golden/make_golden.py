@@ -281,6 +281,31 @@ def make_persistence():
     print("persistence: fields", m.num_fields)
 
 
+def make_propagate():
+    """dynamics.propagate (dynamics.py:305-342) for the analytic, perturbed and hybrid
+    models, mean and sample modes, plus a diverging plan."""
+    p = D.QuadParams()
+    rng = np.random.default_rng(17)
+    plan = C.ControlPlan.hover(p, 30).replaced(
+        np.column_stack([rng.normal(0, 1.5, (30, 3)), p.hover_thrust + rng.normal(0, 0.01, 30)]))
+    state = D.QuadState(np.array([0.2, -0.1, 1.0]), np.array([0.1, 0.0, -0.05]), np.array([0.05, -0.02, 0.3]),
+                        np.zeros(3))
+    noise = rng.standard_normal((30, 3))
+    stacks = synthetic.hybrid_stacks(16, seed=17)
+    hyb = ref_hybrid(stacks)
+    arrays = dict(plan=plan.controls, state=state.as_array(), noise=noise, **stack_arrays("hybrid_", stacks))
+    for name, model, mode in (("analytic", D.AnalyticModel(p), "mean"),
+                              ("perturbed", D.PerturbedModel(p, drag_coeff=0.08, thrust_scale=0.97), "mean"),
+                              ("hybrid_mean", hyb, "mean"), ("hybrid_sample", hyb, "sample")):
+        tr = D.propagate(model, state, plan, 30, mode=mode, noise_seq=noise if mode == "sample" else None)
+        arrays[name + "_states"] = tr.states
+        arrays[name + "_diverged"] = np.array(tr.diverged)
+    wild = plan.replaced(np.tile([0.0, 0.0, 0.0, p.f_max], (30, 1)))  # full thrust: leaves the sanity box
+    tr = D.propagate(D.AnalyticModel(p), state, wild, 30, sanity_box=np.array([1.0, 1.0, 1.5]))
+    arrays["wild_states"], arrays["wild_diverged"] = tr.states, np.array(tr.diverged)
+    save("propagate", **arrays)
+
+
 def make_trial():
     """Closed loop: reference run_trial (simworld.py:270-380), plan with the control
     model, advance a drag/thrust-biased PerturbedModel."""
@@ -312,6 +337,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["nonfinite"]:
         make_nonfinite()
         sys.exit(0)
+    if sys.argv[1:] == ["propagate"]:
+        make_propagate()
+        sys.exit(0)
     make_rng()
     make_lwpr()
     make_eval()
@@ -319,3 +347,4 @@ if __name__ == "__main__":
     make_optimize()
     make_trial()
     make_persistence()
+    make_propagate()

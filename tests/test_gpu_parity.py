@@ -505,3 +505,39 @@ def test_shared_metric_model_from_reference_training():
     scale = max(1.0, float(np.abs(z["mean"]).max()))
     np.testing.assert_allclose(mean, z["mean"], atol=2e-5 * scale)
     np.testing.assert_allclose(var, z["var"], rtol=1e-3, atol=2e-5 * scale)
+
+
+@pytest.mark.parametrize("mode", ["mean", "sample"])
+def test_hybrid_propagate_matches_reference(mode):
+    """dynamics.propagate with the hybrid model (LWPR accelerations on the GPU, float32)
+    against the reference's float64 predictions."""
+    z = load("propagate")
+    p = P.QuadParams()
+    plan = P.ControlPlan(z["plan"], p.dt, 0.0, *p.control_bounds())
+    model = P.HybridModel.from_stacks(stacks_from(z, "hybrid_"), p)
+    tr = P.propagate(model, P.QuadState.from_array(z["state"]), plan, 30, mode=mode,
+                     noise_seq=z["noise"] if mode == "sample" else None)
+    np.testing.assert_allclose(tr.states, z[f"hybrid_{mode}_states"], rtol=1e-4, atol=1e-5)
+    assert tr.diverged == bool(z[f"hybrid_{mode}_diverged"])
+
+
+def test_hybrid_make_batch_eval_protocol():
+    """Model-plugin protocol (dynamics.py:262-277): eval_into fills (B, 3) means and
+    standard deviations from the per-axis LWPR models."""
+    z = load("propagate")
+    p = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks_from(z, "hybrid_"), p)
+    rng = np.random.default_rng(3)
+    X = rng.uniform([-0.3, -0.3, -0.3, 0.12], [0.3, 0.3, 0.3, 0.25], (64, 4)).astype(np.float32)
+    ev = model.make_batch_eval(64)
+    mean, std = np.empty((64, 3), np.float32), np.empty((64, 3), np.float32)
+    ev(X, mean, std)
+    for a in range(3):
+        fr = P.FrozenLwpr(model.models[a], 64)
+        m, v = np.empty(64, np.float32), np.empty(64, np.float32)
+        fr.predict_into(X, m, v)
+        np.testing.assert_array_equal(mean[:, a], m)
+        np.testing.assert_array_equal(std[:, a], np.sqrt(v))
+    mean2 = np.empty((64, 3), np.float32)
+    ev(X, mean2)  # mean-only kernel variant: the same to an ulp
+    np.testing.assert_allclose(mean2, mean, rtol=1e-6, atol=1e-7)

@@ -88,3 +88,44 @@ def test_plant_step_matches_reference_euler():
     nxt = P.AnalyticModel(p).step(st, c)
     np.testing.assert_array_equal(nxt.position, st.position + st.velocity * p.dt)
     np.testing.assert_allclose(nxt.rates, st.rates + p.rate_gain * (c.desired_rates - st.rates) * p.dt)
+
+
+def _propagate_inputs(z):
+    p = P.QuadParams()
+    plan = P.ControlPlan(z["plan"], p.dt, 0.0, *p.control_bounds())
+    return p, plan, P.QuadState.from_array(z["state"])
+
+
+@pytest.mark.parametrize("name", ["analytic", "perturbed"])
+def test_propagate_matches_reference(name):
+    """dynamics.propagate (dynamics.py:305-342) with the host models: bitwise."""
+    z = load("propagate")
+    p, plan, state = _propagate_inputs(z)
+    model = P.AnalyticModel(p) if name == "analytic" else P.PerturbedModel(p, drag_coeff=0.08, thrust_scale=0.97)
+    tr = P.propagate(model, state, plan, 30)
+    np.testing.assert_array_equal(tr.states, z[name + "_states"])
+    assert tr.diverged == bool(z[name + "_diverged"])
+    np.testing.assert_array_equal(tr.positions, tr.states[:, :3])
+    np.testing.assert_array_equal(tr.final_state().as_array(), tr.states[-1])
+    # the same through step_analytic for the analytic model
+    if name == "analytic":
+        s = state
+        for i in range(30):
+            s = P.step_analytic(s, p.control(plan.controls[i, :3], plan.controls[i, 3]), p)
+        np.testing.assert_array_equal(s.as_array(), tr.states[-1])
+
+
+def test_propagate_divergence_and_errors():
+    z = load("propagate")
+    p, plan, state = _propagate_inputs(z)
+    wild = np.tile([0.0, 0.0, 0.0, p.f_max], (30, 1))
+    tr = P.propagate(P.AnalyticModel(p), state, wild, 30, sanity_box=np.array([1.0, 1.0, 1.5]))
+    np.testing.assert_array_equal(tr.states, z["wild_states"])
+    assert tr.diverged and bool(z["wild_diverged"])
+    with pytest.raises(ValueError, match="exceeds plan length"):
+        P.propagate(P.AnalyticModel(p), state, plan, 31)
+    with pytest.raises(ValueError, match="requires noise"):
+        P.propagate(P.AnalyticModel(p), state, plan, 30, mode="sample")
+    with pytest.raises(TypeError, match="velocity-dependent"):
+        P.PerturbedModel(p, drag_coeff=0.1).make_batch_eval(8)
+    assert P.Task.default().total_switches == 3 * 4
