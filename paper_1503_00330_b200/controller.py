@@ -194,6 +194,8 @@ class RolloutEngine:
         self.use_graph = bool(use_graph)
         self._ctxs: dict[tuple[int, int], _abi.Context] = {}
         self._bound: dict[int, tuple] = {}  # per context: key of the dynamics + cost last bound
+        self._io: dict[int, tuple] = {}     # receding_device host buffers per horizon
+        self._args = _abi.OptimizeArgs()
 
     def context(self, num_rollouts: int, horizon: int) -> "_abi.Context":
         key = (int(num_rollouts), int(horizon))
@@ -265,18 +267,40 @@ class RolloutEngine:
 
     def receding_device(self, state: QuadState, plan: ControlPlan, cost_model, cycle_index: int = 0):
         """``receding_horizon_step`` on the GPU with device noise: optimise, then take the
-        first control and shift the plan inside the C ABI (pi2_receding_horizon_step)."""
+        first control and shift the plan inside the C ABI (pi2_receding_horizon_step).
+        Host buffers, their pointers and the argument struct persist across calls
+        (the per-call host overhead is what a real-time loop pays)."""
         cfg = self.config
         if cfg.iterations_per_step > _abi.MAX_ITERATIONS:
             raise ValueError(f"iterations_per_step must be <= {_abi.MAX_ITERATIONS} on the device path")
-        ctx = self.context(cfg.num_rollouts, len(plan))
+        n = len(plan)
+        ctx = self.context(cfg.num_rollouts, n)
         self._bind(ctx, plan, cost_model)
-        controls = np.array(plan.controls, dtype=np.float64, order="C")
-        first = np.empty(4)
-        ctx.call("pi2_receding_horizon_step", _abi.ptr(np.ascontiguousarray(state.as_array())),
-                 _abi.ptr(controls), optimize_args(cfg, cycle_index, self.use_graph), _abi.ptr(first))
+        io = self._io.get(n)
+        if io is None:
+            st, pl, first = np.empty(12), np.empty((n, 4)), np.empty(4)
+            io = self._io[n] = (st, pl, first, _abi.ptr(st), _abi.ptr(pl), _abi.ptr(first))
+        st, pl, first, p_st, p_pl, p_first = io
+        st[0:3], st[3:6], st[6:9], st[9:12] = state.position, state.velocity, state.angles, state.rates
+        pl[...] = plan.controls
+        ctx.call("pi2_receding_horizon_step", p_st, p_pl, self._opt_args(cycle_index), p_first)
         return (Control(first[:3].copy(), float(first[3])),
-                ControlPlan._clipped(controls, plan.dt, plan.origin_time + plan.dt, plan.lo, plan.hi))
+                ControlPlan._clipped(pl.copy(), plan.dt, plan.origin_time + plan.dt, plan.lo, plan.hi))
+
+    def _opt_args(self, cycle_index: int) -> "_abi.OptimizeArgs":
+        """The engine's OptimizeArgs, refreshed from the config (which may be mutated)."""
+        cfg, a = self.config, self._args
+        a.temperature = float(cfg.temperature)
+        a.cost_ceiling = float(cfg.cost_ceiling)
+        std = cfg.exploration_std
+        if a.exploration_std[0] != std[0] or a.exploration_std[1] != std[1] or \
+                a.exploration_std[2] != std[2] or a.exploration_std[3] != std[3]:
+            a.exploration_std[:] = [float(v) for v in std]
+        a.seed = int(cfg.rng_seed) & ((1 << 64) - 1)
+        a.cycle = int(cycle_index) & ((1 << 64) - 1)
+        a.iterations = int(cfg.iterations_per_step)
+        a.use_graph = int(self.use_graph)
+        return a
 
 
 def _cost_key(cost_model):
