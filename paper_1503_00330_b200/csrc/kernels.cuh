@@ -1125,8 +1125,11 @@ __global__ void transpose_costs_kernel(const double *__restrict__ src, double *_
 }
 
 // plan[t] += V/Z of a single partial, clipped (the world-size-1 finalize)
+// plan_host (may be null): the updated plan is also stored there (pinned host memory,
+// device-accessible under unified addressing) -- the last iteration of a host call
+// so no device-to-host copy follows
 __global__ void apply_root_kernel(const double *__restrict__ root, int N, double *__restrict__ plan,
-                                  DynParams dp) {
+                                  DynParams dp, double *plan_host) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 4 * N) return;
@@ -1134,6 +1137,7 @@ __global__ void apply_root_kernel(const double *__restrict__ root, int N, double
   const double *r = root + t * PI2_PARTIAL_WIDTH;
   const double du = __ddiv_rn(__ldcg(r + 2 + c), __ldcg(r + 1));  // coherent (see pdl_wait)
   plan[i] = clip_np(__dadd_rn(plan[i], du), dp.lo[c], dp.hi[c]);
+  if (plan_host) plan_host[i] = plan[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -1156,7 +1160,7 @@ __device__ void smem_tree(double (*v)[PI2_PARTIAL_WIDTH], int n, double neg_inv)
 
 __global__ void __launch_bounds__(256)
     combine_kernel(const double *__restrict__ leaves, int64_t n, int N, double neg_inv,
-                   double *__restrict__ root_out, double *__restrict__ plan, DynParams dp) {
+                   double *__restrict__ root_out, double *__restrict__ plan, DynParams dp, double *plan_host) {
   extern __shared__ double cmb[];
   double(*seg)[PI2_PARTIAL_WIDTH] = reinterpret_cast<double(*)[PI2_PARTIAL_WIDTH]>(cmb);
   double(*roots)[PI2_PARTIAL_WIDTH] = seg + kSeg;
@@ -1189,6 +1193,7 @@ __global__ void __launch_bounds__(256)
       for (int c = 0; c < 4; ++c) {
         const double du = __ddiv_rn(roots[0][2 + c], roots[0][1]);
         plan[4 * t + c] = clip_np(__dadd_rn(plan[4 * t + c], du), dp.lo[c], dp.hi[c]);
+        if (plan_host) plan_host[4 * t + c] = plan[4 * t + c];
       }
     }
   }

@@ -52,6 +52,7 @@ struct pi2_ctx {
   int tc_mode = 1;         // see tc_wanted
   bool tc_stream = false;  // W streamed per chunk (large L)
   bool pdl = true;         // programmatic dependent launch along the step's kernels (PI2_PDL=0: off)
+  bool uva = false;        // pinned host memory is device-accessible (unified addressing)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -491,32 +492,33 @@ dim3 partials_grid(int64_t chunks, int N) {
   return dim3((unsigned)chunks, (unsigned)((N + kChunkWarps - 1) / kChunkWarps));
 }
 
-// after_kernel: the stream predecessor is the partials kernel (PDL allowed)
+// after_kernel: the stream predecessor is the partials kernel (PDL allowed);
+// plan_host: also store the updated plan there (see apply_root_kernel)
 int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
-                   double *plan, cudaStream_t st, bool after_kernel = false) {
+                   double *plan, cudaStream_t st, bool after_kernel = false, double *plan_host = nullptr) {
   if (n == 1 && !root && plan) {  // a single partial: just apply it
-    TRY(launch_pdl_if(after_kernel, ctx, apply_root_kernel, dim3((4 * N + 127) / 128), dim3(128), 0, st, leaves, N, plan, ctx->dp));
+    TRY(launch_pdl_if(after_kernel, ctx, apply_root_kernel, dim3((4 * N + 127) / 128), dim3(128), 0, st, leaves, N, plan, ctx->dp, plan_host));
     CU(cudaGetLastError());
     return PI2_OK;
   }
   if ((n + kSeg - 1) / kSeg > kSeg) return fail(ctx, PI2_ERR_INVALID, "too many partials (%lld)", (long long)n);
   const int smem = 2 * kSeg * PI2_PARTIAL_WIDTH * (int)sizeof(double);
   TRY(set_smem(ctx, combine_kernel, smem));
-  TRY(launch_pdl_if(after_kernel, ctx, combine_kernel, dim3(N), dim3(256), smem, st, leaves, n, N, neg_inv, root, plan, ctx->dp));
+  TRY(launch_pdl_if(after_kernel, ctx, combine_kernel, dim3(N), dim3(256), smem, st, leaves, n, N, neg_inv, root, plan, ctx->dp, plan_host));
   CU(cudaGetLastError());
   return PI2_OK;
 }
 
 // one full device-noise iteration on the device plan (optionally local-only)
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
-                     cudaStream_t st) {
+                     cudaStream_t st, double *plan_host = nullptr) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
   TRY(launch_pdl(ctx, partials_kernel, partials_grid(ctx->n_chunks, ctx->N), dim3(32 * kChunkWarps), 0, st,
                  ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N,
                  neg_inv, ctx->d_partials));
   CU(cudaGetLastError());
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
-                        update_plan ? ctx->d_plan : nullptr, st, true);
+                        update_plan ? ctx->d_plan : nullptr, st, true, plan_host);
 }
 
 int validate_opt(pi2_ctx *ctx, const pi2_optimize_args *args) {
@@ -600,6 +602,11 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (const char *e = getenv("PI2_PDL")) ctx->pdl = std::atoi(e) != 0;
+  {
+    int uva = 0;
+    cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
+    ctx->uva = uva != 0;
+  }
   if (const char *e = getenv("PI2_LWPR_TC")) {
     ctx->tc_mode = std::atoi(e);
     ctx->tc_enabled = ctx->tc_mode != 0;
@@ -831,8 +838,11 @@ int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const dou
 static int enqueue_iterations(pi2_ctx *ctx, int iterations, double neg_inv, bool io, cudaStream_t st) {
   const size_t plan_bytes = sizeof(double) * 4 * ctx->N;
   if (io) CU(cudaMemcpyAsync(ctx->d_io, ctx->h_io, kIoArgsBytes + plan_bytes, cudaMemcpyHostToDevice, st));
-  for (int it = 0; it < iterations; ++it) TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st));
-  if (io) CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, plan_bytes, cudaMemcpyDeviceToHost, st));
+  // the last iteration's update also lands in the pinned host plan (no D2H copy node)
+  const bool direct = io && ctx->uva;
+  for (int it = 0; it < iterations; ++it)
+    TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st, direct && it == iterations - 1 ? ctx->h_plan : nullptr));
+  if (io && !direct) CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, plan_bytes, cudaMemcpyDeviceToHost, st));
   return PI2_OK;
 }
 
