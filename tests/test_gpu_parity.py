@@ -82,7 +82,9 @@ def test_evaluate_matches_reference_golden(name):
                                           (20000, 30, 24, 1, False), (20000, 24, 24, 4, False),
                                           (17000, 20, 16, 3, True),
                                           # tensor-core LWPR chunking: 64 + 64 + 2 fields, one full chunk
-                                          (20000, 12, 130, 1, False), (17000, 10, 64, 4, False)])
+                                          (20000, 12, 130, 1, False), (17000, 10, 64, 4, False),
+                                          # M > 32: the generic kernel (pairwise halving 40 -> 5, then a mean)
+                                          (600, 10, 16, 40, False), (300, 8, 12, 64, False)])
 def test_evaluate_matches_oracle(K, N, L, M, full):
     stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
     params = P.QuadParams()
