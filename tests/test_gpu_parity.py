@@ -84,7 +84,10 @@ def test_evaluate_matches_reference_golden(name):
                                           # tensor-core LWPR chunking: 64 + 64 + 2 fields, one full chunk
                                           (20000, 12, 130, 1, False), (17000, 10, 64, 4, False),
                                           # M > 32: the generic kernel (pairwise halving 40 -> 5, then a mean)
-                                          (600, 10, 16, 40, False), (300, 8, 12, 64, False)])
+                                          (600, 10, 16, 40, False), (300, 8, 12, 64, False),
+                                          # long horizons: shared-memory footprints scale with N
+                                          (2000, 300, 16, 1, False), (17000, 300, 16, 1, False),
+                                          (3000, 300, 16, 4, False)])
 def test_evaluate_matches_oracle(K, N, L, M, full):
     stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
     params = P.QuadParams()
@@ -101,7 +104,12 @@ def test_evaluate_matches_oracle(K, N, L, M, full):
     rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise,
                          RO.Cost(TASK_WAYPOINTS[2], TASK_OBSTACLES), dyn, M)
     np.testing.assert_array_equal(b.crash_flags, rf)
-    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+    if N <= 100:  # BASELINE horizons go to T = 100
+        assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+    else:  # the gate on the first 100 steps; beyond, float32 trajectory drift (in the reference
+        # itself) of rollouts flown far outside the model's support grows: 300 steps reach ~1.2e-5
+        assert cost_rel_err(b.costs_to_go[:, :100], rc[:, :100]) < COST_RTOL
+        assert cost_rel_err(b.costs_to_go, rc) < 5e-5
     new = P.path_integral_update(plan, b, 1.0)
     assert np.all(du_err(new.controls, RO.update(plan.controls, lo, hi, rc, noise, 1.0), plan.controls) < DU_TOL)
 
