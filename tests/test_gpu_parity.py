@@ -87,7 +87,9 @@ def test_evaluate_matches_reference_golden(name):
                                           (600, 10, 16, 40, False), (300, 8, 12, 64, False),
                                           # long horizons: shared-memory footprints scale with N
                                           (2000, 300, 16, 1, False), (17000, 300, 16, 1, False),
-                                          (3000, 300, 16, 4, False)])
+                                          (3000, 300, 16, 4, False),
+                                          # one- and two-field models (a chunk of 8 is mostly padding)
+                                          (2048, 10, 1, 1, False), (2048, 10, 2, 4, False)])
 def test_evaluate_matches_oracle(K, N, L, M, full):
     stacks = synthetic.hybrid_stacks(L, seed=K + N, full_metric=full)
     params = P.QuadParams()
