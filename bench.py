@@ -50,7 +50,7 @@ KERNELS_PER_ITER = 5  # attitude, lwpr, rollout, partials, combine
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="C2")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -137,33 +137,79 @@ def cpu_model() -> str:
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi samples during the timed region (SM clock, max clock, throttle reasons)."""
+    """SM clock, max clock and throttle reasons sampled DURING the timed region.
 
+    NVML (nvidia_ml_py) is polled every ~2 ms from a thread, so even a
+    millisecond-scale timed region gets samples; only samples between mark_start()
+    and mark_end() (the caller's timed window) are summarised.  Falls back to
+    `nvidia-smi -lms 100` when NVML is unavailable."""
+
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple] = []  # (t, sm_mhz, max_mhz, reasons)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.proc = self.thread = None
+        self.source = None
+
+    def mark_start(self):
+        self.t0 = time.monotonic()
+
+    def mark_end(self):
+        self.t1 = time.monotonic()
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((time.monotonic(), float(sm), float(mx),
+                                         tuple(n for n, b in zip(self.REASONS, bits) if r & b)))
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            self.source = "nvml"
+            return self
+        except Exception:  # noqa: BLE001 - no NVML: nvidia-smi
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
             self.thread.start()
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                sm, mx = float(parts[0]), float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            reasons = tuple(n for n, v in zip(self.REASONS, parts[4:8]) if v.lower().startswith("active"))
+            self.samples.append((time.monotonic(), sm, mx, reasons))
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -171,27 +217,17 @@ class ClockSampler:
                 self.proc.wait(timeout=2)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread is not None:
             self.thread.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        inside = [s for s in self.samples if self.t0 is not None and self.t1 is not None and self.t0 <= s[0] <= self.t1]
+        use = inside or self.samples
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
+        reasons = sorted({r for s in use for r in s[3]})
+        return {"sm_mhz": statistics.median(s[1] for s in use), "sm_max_mhz": max(s[2] for s in use),
+                "reasons": reasons, "samples": len(use), "in_timed_region": bool(inside), "source": self.source}
 
 
 # ---------------------------------------------------------------- ours
@@ -291,11 +327,15 @@ def run_ours(args, rank: int, world: int, local: int):
     barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        clocks.mark_start()
         start.record(stream)
         for s in range(args.steps):
             device_step(s)
         end.record(stream)
+        while not end.query():  # a sleeping wait keeps the GIL free for the clock sampler
+            time.sleep(0.0005)
         barrier()
+        clocks.mark_end()
     dev_ms = max_over_ranks(start.elapsed_time(end))
     ms_per_step = dev_ms / args.steps
     value = K * T * args.steps / (dev_ms / 1e3)
