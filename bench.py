@@ -424,7 +424,8 @@ def run_ours(args, rank: int, world: int, local: int):
         "higher_is_better": True,
         "scaling": args.scaling,
         "vs_baseline": None,
-        "dtype": "f32 (LWPR, integration, cost) + f64 (attitude, cost-to-go, update)",
+        "dtype": "f32 (LWPR: linear parts as 3xTF32 tcgen05 products with f32 accumulation, exp/moments f32; "
+                 "integration, cost) + f64 (attitude, cost-to-go, update)",
         "data": "synthetic (seeded hybrid-LWPR model linearising the rigid-body quadrotor; device Philox noise)",
         "config": {
             "workload": f"{args.config}: {desc}" + (f" (x{world} GPUs, weak scaling: K per GPU)"
