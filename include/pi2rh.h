@@ -33,7 +33,6 @@ extern "C" {
 
 #define PI2_ABI_VERSION 1
 #define PI2_MAX_OBSTACLES 16
-#define PI2_MAX_ITERATIONS 16
 #define PI2_MAX_SUB_ROLLOUTS 64
 #define PI2_PARTIAL_WIDTH 6 /* (min S, Z, V[4]) per timestep, float64 */
 
@@ -99,7 +98,7 @@ typedef struct pi2_optimize_args {
   double exploration_std[4];
   uint64_t seed;
   uint64_t cycle;
-  int32_t iterations; /* 0..PI2_MAX_ITERATIONS */
+  int32_t iterations; /* >= 0; keys are derived per iteration on the device */
   int32_t use_graph;  /* capture/replay the whole step as one CUDA graph */
 } pi2_optimize_args;
 

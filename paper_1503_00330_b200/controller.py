@@ -255,8 +255,6 @@ class RolloutEngine:
                         cycle_index: int = 0) -> ControlPlan:
         """All ``iterations_per_step`` iterations on the GPU with device noise (one CUDA graph)."""
         cfg = self.config
-        if cfg.iterations_per_step > _abi.MAX_ITERATIONS:
-            raise ValueError(f"iterations_per_step must be <= {_abi.MAX_ITERATIONS} on the device path")
         ctx = self.context(cfg.num_rollouts, len(plan))
         self._bind(ctx, plan, cost_model)
         controls = np.ascontiguousarray(plan.controls, dtype=np.float64).copy()
@@ -264,15 +262,12 @@ class RolloutEngine:
                  optimize_args(cfg, cycle_index, self.use_graph))
         return plan.replaced(controls)
 
-
     def receding_device(self, state: QuadState, plan: ControlPlan, cost_model, cycle_index: int = 0):
         """``receding_horizon_step`` on the GPU with device noise: optimise, then take the
         first control and shift the plan inside the C ABI (pi2_receding_horizon_step).
         Host buffers, their pointers and the argument struct persist across calls
         (the per-call host overhead is what a real-time loop pays)."""
         cfg = self.config
-        if cfg.iterations_per_step > _abi.MAX_ITERATIONS:
-            raise ValueError(f"iterations_per_step must be <= {_abi.MAX_ITERATIONS} on the device path")
         n = len(plan)
         ctx = self.context(cfg.num_rollouts, n)
         self._bind(ctx, plan, cost_model)

@@ -54,7 +54,10 @@ constexpr int kLayDiag = 0, kLayFull = 1, kLayShared = 2;
 // replays pick up new state / keys / cost without re-capture).
 struct StepArgs {
   double state[12];
-  uint64_t keys[PI2_MAX_ITERATIONS][2][2];  // [iteration][control|dynamics][k0,k1]
+  // [control|dynamics]: the (seed, stream, cycle) links of the key chain; each
+  // kernel derives its iteration's key itself (iter_key), so any iteration count
+  // runs from one staged StepArgs
+  uint64_t key_prefix[2];
   double std[4];
   double neg_inv_temp;  // -1 / temperature (controller.py:368)
   double ceiling;       // cost_ceiling (controller.py:243-246)
@@ -102,14 +105,29 @@ PI2_HD uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-inline void derive_key(uint64_t seed, uint64_t stream, uint64_t cycle, uint64_t iteration,
-                       uint64_t out[2]) {
+// 128-bit Philox key of one stream address
+struct Key128 {
+  uint64_t k0, k1;
+};
+
+// first links of the chain: (seed, stream, cycle)
+inline uint64_t key_prefix(uint64_t seed, uint64_t stream, uint64_t cycle) {
   uint64_t h = splitmix64(seed);
   h = splitmix64(h ^ stream);
-  h = splitmix64(h ^ cycle);
-  h = splitmix64(h ^ iteration);
-  out[0] = splitmix64(h);
-  out[1] = splitmix64(h ^ 0xA5A5A5A5A5A5A5A5ull);
+  return splitmix64(h ^ cycle);
+}
+
+// last links: the key of optimisation iteration `it` under a prefix
+PI2_HD Key128 iter_key(uint64_t prefix, uint64_t it) {
+  const uint64_t h = splitmix64(prefix ^ it);
+  return Key128{splitmix64(h), splitmix64(h ^ 0xA5A5A5A5A5A5A5A5ull)};
+}
+
+inline void derive_key(uint64_t seed, uint64_t stream, uint64_t cycle, uint64_t iteration,
+                       uint64_t out[2]) {
+  const Key128 k = iter_key(key_prefix(seed, stream, cycle), iteration);
+  out[0] = k.k0;
+  out[1] = k.k1;
 }
 
 }  // namespace pi2

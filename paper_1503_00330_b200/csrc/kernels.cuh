@@ -69,9 +69,10 @@ __device__ __forceinline__ float4 normals4(uint64_t index, uint64_t k0, uint64_t
 }
 
 // exploration noise eps[k, t, :] of the device stream (float32 normals x float64 std)
-__device__ __forceinline__ void device_eps(const StepArgs *sa, int it, uint64_t kg, int N, int t,
+// (key: iter_key(sa->key_prefix[0], iteration), derived once per thread)
+__device__ __forceinline__ void device_eps(const StepArgs *sa, Key128 key, uint64_t kg, int N, int t,
                                            double e[4]) {
-  const float4 z = normals4(kg * (uint64_t)N + (uint64_t)t, sa->keys[it][0][0], sa->keys[it][0][1]);
+  const float4 z = normals4(kg * (uint64_t)N + (uint64_t)t, key.k0, key.k1);
   e[0] = __dmul_rn((double)z.x, sa->std[0]);
   e[1] = __dmul_rn((double)z.y, sa->std[1]);
   e[2] = __dmul_rn((double)z.z, sa->std[2]);
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kRolloutBlock)
   double ang[3] = {sa->state[6], sa->state[7], sa->state[8]};
   double rate[3] = {sa->state[9], sa->state[10], sa->state[11]};
   const double *ek = DEVICE_NOISE ? nullptr : eps + k * (int64_t)N * 4;
+  const Key128 ck = DEVICE_NOISE ? iter_key(sa->key_prefix[0], (uint64_t)iteration) : Key128{0, 0};
   float4 *xk = xin + k;  // row (k, t) at xk[t * K]
   constexpr int TB = 4;  // noise of TB steps is generated before their serial FP64 recurrence
   for (int t0 = 0; t0 < N; t0 += TB) {
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kRolloutBlock)
     for (int j = 0; j < TB; ++j) {
       const int t = t0 + j < N ? t0 + j : N - 1;
       if (DEVICE_NOISE) {
-        device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e[j]);
+        device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e[j]);
       } else {
         const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
         const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
@@ -583,7 +585,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
                        __double2float_rn(sa->state[2])};
   const float v0[3] = {__double2float_rn(sa->state[3]), __double2float_rn(sa->state[4]),
                        __double2float_rn(sa->state[5])};
-  const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
+  const Key128 dkey = iter_key(sa->key_prefix[1], (uint64_t)a.iteration);
+  const uint64_t dk0 = dkey.k0, dk1 = dkey.k1;
   const uint64_t kg = (uint64_t)(a.k_off + k);
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
@@ -753,7 +756,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
                        __double2float_rn(sa->state[2])};
   const float v0[3] = {__double2float_rn(sa->state[3]), __double2float_rn(sa->state[4]),
                        __double2float_rn(sa->state[5])};
-  const uint64_t dk0 = sa->keys[a.iteration][1][0], dk1 = sa->keys[a.iteration][1][1];
+  const Key128 dkey = iter_key(sa->key_prefix[1], (uint64_t)a.iteration);
+  const uint64_t dk0 = dkey.k0, dk1 = dkey.k1;
   const uint64_t kg = (uint64_t)(a.k_off + k);
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const pi2_cost &nav = cost;
@@ -913,10 +917,11 @@ __global__ void __launch_bounds__(32 * kWideWarps)
   __syncthreads();
   const int64_t k = (int64_t)blockIdx.x * kWideWarps + warp;
   if (k >= K) return;
+  const Key128 ck = DEVICE_NOISE ? iter_key(sa->key_prefix[0], (uint64_t)iteration) : Key128{0, 0};
   for (int t = lane; t < N; t += 32) {
     double e[4];
     if (DEVICE_NOISE) {
-      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+      device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e);
     } else {
       const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
       const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
@@ -1079,6 +1084,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
   }
   m = warp_min(m);
   double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
+  const Key128 ck = eps ? Key128{0, 0} : iter_key(sa->key_prefix[0], (uint64_t)iteration);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int64_t k = k0 + lane + 32 * j;
@@ -1090,7 +1096,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
       const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
       e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
     } else {
-      device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+      device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e);
     }
     z = __dadd_rn(z, w);
 #pragma unroll
@@ -1208,7 +1214,7 @@ __global__ void shift_plan_kernel(const double *__restrict__ src, double *__rest
 }
 
 // device noise materialisation (tests / RolloutBatch.noise of device mode)
-__global__ void noise_kernel(const StepArgs *__restrict__ sa, int which, int iteration, int64_t K,
+__global__ void noise_kernel(const StepArgs *__restrict__ sa, int which, uint64_t iteration, int64_t K,
                              int64_t k_off, int N, int M, double *__restrict__ eps_out,
                              float *__restrict__ dyn_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1217,13 +1223,14 @@ __global__ void noise_kernel(const StepArgs *__restrict__ sa, int which, int ite
     const int64_t k = i / N;
     const int t = (int)(i % N);
     double e[4];
-    device_eps(sa, iteration, (uint64_t)(k_off + k), N, t, e);
+    device_eps(sa, iter_key(sa->key_prefix[0], iteration), (uint64_t)(k_off + k), N, t, e);
 #pragma unroll
     for (int c = 0; c < 4; ++c) eps_out[i * 4 + c] = e[c];
   } else {
     if (i >= K * M * N) return;  // i = (k * M + m) * N + t
     const uint64_t kg_idx = (uint64_t)(k_off * M * N + i);
-    const float4 z = normals4(kg_idx, sa->keys[iteration][1][0], sa->keys[iteration][1][1]);
+    const Key128 dk = iter_key(sa->key_prefix[1], iteration);
+    const float4 z = normals4(kg_idx, dk.k0, dk.k1);
     dyn_out[i * 3 + 0] = z.x;
     dyn_out[i * 3 + 1] = z.y;
     dyn_out[i * 3 + 2] = z.z;

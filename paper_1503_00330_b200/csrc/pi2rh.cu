@@ -402,10 +402,8 @@ void fill_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, 
     h.neg_inv_temp = -1.0 / opt->temperature;
     h.ceiling = opt->cost_ceiling;
     for (int c = 0; c < 4; ++c) h.std[c] = opt->exploration_std[c];
-    for (int it = 0; it < std::max(1, opt->iterations) && it < PI2_MAX_ITERATIONS; ++it) {
-      derive_key(opt->seed, PI2_STREAM_CONTROL, opt->cycle, (uint64_t)it, h.keys[it][0]);
-      derive_key(opt->seed, PI2_STREAM_DYNAMICS, opt->cycle, (uint64_t)it, h.keys[it][1]);
-    }
+    h.key_prefix[0] = key_prefix(opt->seed, PI2_STREAM_CONTROL, opt->cycle);
+    h.key_prefix[1] = key_prefix(opt->seed, PI2_STREAM_DYNAMICS, opt->cycle);
   }
 }
 
@@ -526,8 +524,7 @@ int validate_opt(pi2_ctx *ctx, const pi2_optimize_args *args) {
   if (!(args->temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
   for (double s : args->exploration_std)
     if (!(s > 0)) return fail(ctx, PI2_ERR_INVALID, "exploration_std must be positive");
-  if (args->iterations < 0 || args->iterations > PI2_MAX_ITERATIONS)
-    return fail(ctx, PI2_ERR_INVALID, "iterations must be in [0, %d]", PI2_MAX_ITERATIONS);
+  if (args->iterations < 0) return fail(ctx, PI2_ERR_INVALID, "iterations must be >= 0");
   return PI2_OK;
 }
 
@@ -1077,8 +1074,8 @@ int pi2_device_noise(pi2_ctx *ctx, int32_t which, uint64_t seed, uint64_t cycle,
   CU(cudaEventSynchronize(ctx->staged));
   StepArgs &h = *ctx->h_args;
   for (int c = 0; c < 4; ++c) h.std[c] = a.exploration_std[c];
-  derive_key(seed, PI2_STREAM_CONTROL, cycle, iteration, h.keys[0][0]);
-  derive_key(seed, PI2_STREAM_DYNAMICS, cycle, iteration, h.keys[0][1]);
+  h.key_prefix[0] = key_prefix(seed, PI2_STREAM_CONTROL, cycle);
+  h.key_prefix[1] = key_prefix(seed, PI2_STREAM_DYNAMICS, cycle);
   CU(cudaMemcpyAsync(ctx->d_args, ctx->h_args, sizeof(StepArgs), cudaMemcpyHostToDevice, st));
   CU(cudaEventRecord(ctx->staged, st));
   const int64_t K = ctx->K, N = ctx->N, M = ctx->M;
@@ -1086,7 +1083,7 @@ int pi2_device_noise(pi2_ctx *ctx, int32_t which, uint64_t seed, uint64_t cycle,
   const size_t bytes = which == PI2_STREAM_CONTROL ? sizeof(double) * n * 4 : sizeof(float) * n * 3;
   TRY(ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, bytes));
   noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      ctx->d_args, which, 0, K, ctx->dims.rollout_offset, (int)N, (int)M, (double *)ctx->d_scratch,
+      ctx->d_args, which, iteration, K, ctx->dims.rollout_offset, (int)N, (int)M, (double *)ctx->d_scratch,
       (float *)ctx->d_scratch);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(out_host, ctx->d_scratch, bytes, cudaMemcpyDeviceToHost, st));

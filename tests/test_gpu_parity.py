@@ -314,6 +314,28 @@ def test_device_noise_statistics_and_addressing():
     assert abs(np.mean(z ** 4) - 3.0) < 0.05  # Gaussian kurtosis
 
 
+@pytest.mark.parametrize("seed,cycle,it", [(7, 3, 1), (11, 0, 17), (5, 2, 1000)])
+def test_device_noise_matches_host_replica(seed, cycle, it):
+    """The device streams are Philox4x32-10 under rng.derive_key(seed, stream, cycle, it):
+    the kernels derive the iteration's key themselves from StepArgs.key_prefix."""
+    from tests import devnoise
+    K, N, M = 300, 20, 3
+    cfg = P.PiConfig(num_rollouts=K, horizon_steps=N, sub_rollouts=M)
+    eng = P.RolloutEngine(P.AnalyticModel(P.QuadParams()), cfg, device=0, noise="device")
+    ctx = eng.context(K, N)
+    std = np.array([1.5, 1.5, 0.6, 0.04])
+    eps = np.empty((K, N, 4))
+    ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, seed, cycle, it, _abi.ptr(std), _abi.ptr(eps))
+    dyn = np.empty((K, M, N, 3), np.float32)
+    ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, seed, cycle, it, None, _abi.ptr(dyn))
+    # MUFU lg2/sin/cos approximations: ~1e-6 typically, up to ~1e-4 where u1 -> 1 (r -> 0);
+    # a wrong key or counter gives O(1) differences everywhere
+    for dev, host in ((eps / std, devnoise.control_noise(seed, cycle, it, K, N, std) / std),
+                      (dyn, devnoise.dynamics_noise(seed, cycle, it, K, M, N))):
+        err = np.abs(dev - host)
+        assert err.max() < 5e-4 and np.median(err) < 2e-6, (err.max(), np.median(err))
+
+
 def _device_setup(K=3000, N=40, L=48, M=4, iters=2):
     params = P.QuadParams()
     model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=9), params)
@@ -341,6 +363,27 @@ def test_device_optimize_equals_materialised_noise_path():
     rc, _ = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, eps,
                         RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES), dyn, cfg.sub_rollouts)
     assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_device_optimize_beyond_sixteen_iterations(use_graph):
+    """iterations_per_step is unbounded on the device path (reference PiConfig has no cap):
+    20 fused iterations == 20 rounds of evaluate + update on the materialised device noise."""
+    params, model, cfg, task, state, plan, cost = _device_setup(K=1000, N=20, iters=20)
+    cyc = 2
+    fused = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=use_graph).optimize_device(
+        state, plan, cost, cycle_index=cyc)
+    eng = P.RolloutEngine(model, cfg, device=0)
+    ctx = eng.context(cfg.num_rollouts, cfg.horizon_steps)
+    p = plan
+    for it in range(cfg.iterations_per_step):
+        eps = np.empty((cfg.num_rollouts, cfg.horizon_steps, 4))
+        ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, cfg.rng_seed, cyc, it, _abi.ptr(cfg.exploration_std),
+                 _abi.ptr(eps))
+        dyn = np.empty((cfg.num_rollouts, cfg.sub_rollouts, cfg.horizon_steps, 3), np.float32)
+        ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, cfg.rng_seed, cyc, it, None, _abi.ptr(dyn))
+        p = P.path_integral_update(p, eng.evaluate(state, p, eps, cost, dyn), cfg.temperature)
+    np.testing.assert_array_equal(fused.controls, p.controls)
 
 
 def test_graph_replay_matches_eager_and_is_deterministic():
