@@ -1134,6 +1134,15 @@ __global__ void transpose_costs_kernel(const double *__restrict__ src, double *_
 // plan_host (may be null): the updated plan is also stored there (pinned host memory,
 // device-accessible under unified addressing) -- the last iteration of a host call
 // so no device-to-host copy follows
+// The step's inputs (StepArgs + plan) pulled from pinned host memory over
+// unified addressing at the head of the I/O graph, instead of a copy-engine
+// node.  No early trigger: every later kernel of the step starts after these
+// writes are complete.  Volatile loads: the host rewrites the block between
+// replays.
+__global__ void io_pull_kernel(const uint4 *src_host, uint4 *__restrict__ dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcv(src_host + i);
+}
+
 __global__ void apply_root_kernel(const double *__restrict__ root, int N, double *__restrict__ plan,
                                   DynParams dp, double *plan_host) {
   pdl_wait();

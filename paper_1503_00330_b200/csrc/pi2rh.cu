@@ -53,6 +53,7 @@ struct pi2_ctx {
   bool tc_stream = false;  // W streamed per chunk (large L)
   bool pdl = true;         // programmatic dependent launch along the step's kernels (PI2_PDL=0: off)
   bool uva = false;        // pinned host memory is device-accessible (unified addressing)
+  bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -425,8 +426,11 @@ int stage_plan(pi2_ctx *ctx, const double *plan, cudaStream_t st) {
 }
 
 // rollouts of one iteration: attitude -> LWPR -> rollout/cost
+// att_pdl: the attitude kernel may be a programmatic dependent launch (its stream
+// predecessor is a kernel whose outputs it reads only after pdl_wait)
 int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const float *dyn_dev,
-                    double *costs, uint8_t *crash, cudaStream_t st, cudaEvent_t *ev = nullptr) {
+                    double *costs, uint8_t *crash, cudaStream_t st, cudaEvent_t *ev = nullptr,
+                    bool att_pdl = false) {
   const int64_t K = ctx->K;
   const int N = ctx->N;
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
@@ -436,23 +440,23 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
     const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
     if (noise_dev) {
       TRY(set_smem(ctx, attitude_wide_kernel<false>, wsmem));
-      TRY(launch_pdl_if(false, ctx, attitude_wide_kernel<false>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
+      TRY(launch_pdl_if(att_pdl, ctx, attitude_wide_kernel<false>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
                      ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
                      ctx->d_ang_last));
     } else {
       TRY(set_smem(ctx, attitude_wide_kernel<true>, wsmem));
-      TRY(launch_pdl_if(false, ctx, attitude_wide_kernel<true>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
+      TRY(launch_pdl_if(att_pdl, ctx, attitude_wide_kernel<true>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
                      ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
                      ctx->d_ang_last));
     }
   } else if (noise_dev) {
     TRY(set_smem(ctx, attitude_kernel<false>, psmem));
-    TRY(launch_pdl_if(false, ctx, attitude_kernel<false>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+    TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<false>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
                    noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last,
                    nullptr));
   } else {
     TRY(set_smem(ctx, attitude_kernel<true>, psmem));
-    TRY(launch_pdl_if(false, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+    TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
                    nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, nullptr));
   }
   CU(cudaGetLastError());
@@ -509,8 +513,8 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 
 // one full device-noise iteration on the device plan (optionally local-only)
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
-                     cudaStream_t st, double *plan_host = nullptr) {
-  TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st));
+                     cudaStream_t st, double *plan_host = nullptr, bool att_pdl = false) {
+  TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, nullptr, att_pdl));
   TRY(launch_pdl(ctx, partials_kernel, partials_grid(ctx->n_chunks, ctx->N), dim3(32 * kChunkWarps), 0, st,
                  ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N,
                  neg_inv, ctx->d_partials));
@@ -599,6 +603,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if ((rc = bind(ctx)) != PI2_OK) { g_noctx_err = ctx->err; return cleanup(rc); }
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (const char *e = getenv("PI2_PDL")) ctx->pdl = std::atoi(e) != 0;
+  if (const char *e = getenv("PI2_IO_PULL")) ctx->io_pull = std::atoi(e) != 0;
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
@@ -834,11 +839,19 @@ int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const dou
 // io: also copy StepArgs + plan in from the pinned block first and the plan back out last
 static int enqueue_iterations(pi2_ctx *ctx, int iterations, double neg_inv, bool io, cudaStream_t st) {
   const size_t plan_bytes = sizeof(double) * 4 * ctx->N;
-  if (io) CU(cudaMemcpyAsync(ctx->d_io, ctx->h_io, kIoArgsBytes + plan_bytes, cudaMemcpyHostToDevice, st));
+  const bool pull = io && ctx->uva && ctx->io_pull;
+  if (pull) {
+    io_pull_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint4 *>(ctx->h_io), reinterpret_cast<uint4 *>(ctx->d_io),
+                                      (int)((kIoArgsBytes + plan_bytes) / sizeof(uint4)));
+    CU(cudaGetLastError());
+  } else if (io) {
+    CU(cudaMemcpyAsync(ctx->d_io, ctx->h_io, kIoArgsBytes + plan_bytes, cudaMemcpyHostToDevice, st));
+  }
   // the last iteration's update also lands in the pinned host plan (no D2H copy node)
   const bool direct = io && ctx->uva;
   for (int it = 0; it < iterations; ++it)
-    TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st, direct && it == iterations - 1 ? ctx->h_plan : nullptr));
+    TRY(launch_iteration(ctx, it, neg_inv, nullptr, true, st, direct && it == iterations - 1 ? ctx->h_plan : nullptr,
+                         pull && it == 0));
   if (io && !direct) CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, plan_bytes, cudaMemcpyDeviceToHost, st));
   return PI2_OK;
 }
