@@ -221,7 +221,7 @@ class RolloutEngine:
         p = self.params
         key = (p.mass, p.gravity, p.rate_gain, p.dt, np.asarray(plan.lo, float).tobytes(),
                np.asarray(plan.hi, float).tobytes(), _cost_key(cost_model))
-        if key[-1] is not None and self._bound.get(id(ctx)) == key:
+        if self._bound.get(id(ctx)) == key and key[-1] is not None:
             return
         self._bound.pop(id(ctx), None)
         ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
@@ -301,14 +301,16 @@ class RolloutEngine:
 def _cost_key(cost_model):
     """Value key of a cost plugin's device descriptor (see simworld.cost_struct); None when
     the plugin has no device form (cost_struct then raises)."""
-    if all(hasattr(cost_model, a) for a in ("waypoint", "obstacles", "z_floor", "lo", "hi")):
-        f32 = np.float32
-        return ("nav", np.asarray(cost_model.waypoint, f32).tobytes(), np.asarray(cost_model.obstacles, f32).tobytes(),
-                float(np.float32(cost_model.z_floor)), np.asarray(cost_model.lo, f32).tobytes(),
-                np.asarray(cost_model.hi, f32).tobytes())
-    if hasattr(cost_model, "threshold") and not hasattr(cost_model, "waypoint"):
-        return ("threshold", float(np.float32(cost_model.threshold)))
-    return None
+    try:
+        wp, obs, zf = cost_model.waypoint, cost_model.obstacles, cost_model.z_floor
+        lo, hi = cost_model.lo, cost_model.hi
+    except AttributeError:
+        if hasattr(cost_model, "threshold") and not hasattr(cost_model, "waypoint"):
+            return ("threshold", float(np.float32(cost_model.threshold)))
+        return None
+    f32 = np.float32
+    return ("nav", np.asarray(wp, f32).tobytes(), np.asarray(obs, f32).tobytes(), float(f32(zf)),
+            np.asarray(lo, f32).tobytes(), np.asarray(hi, f32).tobytes())
 
 
 def optimize_args(cfg: PiConfig, cycle_index: int, use_graph: bool = True) -> "_abi.OptimizeArgs":
