@@ -44,6 +44,7 @@ constexpr int kTcTmemCols = 2 * PI2_TC_CHUNK;  // power of two >= 32
 
 constexpr int kTcMaxChunks = 32;    // fields per axis <= 32 * kTcChunk on this path
 constexpr int kTcWSlotFloats = 2 * 2 * kTcChunk * 8;  // W of one chunk (hi + lo), streamed mode slot
+constexpr int kTcBulkMaxTiles = 16;  // tiles per CTA up to which resident W arrives by bulk copy (WBULK)
 
 struct LwprTcArgs {
   const float *w;        // per axis, per chunk: W_hi then W_lo, each (2*Lc_pad rows x 8) in UMMA layout,
@@ -263,7 +264,12 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
 // STREAM: the axis' W does not fit in shared memory next to 3 other CTAs (large L):
 // each chunk's W (<= 8 KB, L2-resident, read by every CTA of the axis) is brought in
 // by a TMA bulk copy into a 2-slot ring, one chunk ahead of its MMA.
-template <bool VAR, bool STREAM>
+// WBULK (resident W, few tiles per CTA): the resident block arrives by one bulk copy
+// issued before pdl_wait instead of an LDG/STS loop.  With few tiles that prologue is
+// on the critical path: CTAs that become resident only when the attitude kernel's
+// blocks leave the SM run it after the attitude kernel.  With many tiles the loop is
+// amortised, and that instantiation keeps its own (faster) register allocation.
+template <bool VAR, bool STREAM, bool WBULK = false>
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprTcArgs a) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ uint32_t tmem_base;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   uint8_t *sa = tsm + (((wfl + nlv) * 4 + 127) / 128) * 128;  // two A operands
   const int tid = threadIdx.x, warp = tid >> 5;
 
-  if (!STREAM)
+  if (!STREAM && !WBULK)
     for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
       reinterpret_cast<float4 *>(sw)[i] = __ldg(reinterpret_cast<const float4 *>(a.w + wbeg) + i);
   for (int64_t i = tid; i < nlv; i += blockDim.x) slv_base[i] = __ldg(a.w + a.lv_off[ax] + i);
@@ -307,12 +313,23 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   const uint32_t mbar_addr = (uint32_t)__cvta_generic_to_shared(&mbar);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_addr));
-    if (STREAM) {
+    if (STREAM || WBULK) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr + 8));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
-    if (STREAM && blockIdx.x / 3 < (a.rows + 127) / 128) load_w(0, 0);
+    if ((STREAM || WBULK) && blockIdx.x / 3 < (a.rows + 127) / 128) {
+      if (STREAM) {
+        load_w(0, 0);
+      } else {  // the whole resident block, waited for before the first MMA
+        const uint32_t bytes = (uint32_t)((wend - wbeg) * 4);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wbar_addr), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sw_addr0),
+            "l"(a.w + wbeg), "r"(bytes), "r"(wbar_addr)
+            : "memory");
+      }
+    }
   }
   const AxisHeader &h = a.axis[ax];
   const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
@@ -345,6 +362,8 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   long long prof[5] = {0, 0, 0, 0, 0}, t_last = clock64();
 #endif
 
+  // WBULK: the resident W landed (thread 0 issues every MMA)
+  if (WBULK && tid == 0 && tile < ntiles) mbar_wait(wbar_addr, 0);
   for (; tile < ntiles; tile += tstride, buf ^= 1) {
     const uint32_t sa_addr = (uint32_t)__cvta_generic_to_shared(sa + buf * kTcABytes);
     float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;

@@ -251,12 +251,16 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   a.sd_out = sd_out;
   a.plane = rows;
   a.sqrt_out = 1;
-  auto *fn = ctx->tc_stream ? lwpr_tc_kernel<VAR, true> : lwpr_tc_kernel<VAR, false>;
-  TRY(set_smem(ctx, fn, ctx->tc_smem));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const int64_t tiles = (rows + 127) / 128;
-  const int64_t grid = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles) * 3;  // CTA i -> axis i % 3
+  const int64_t per_axis = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles);
+  const int64_t grid = per_axis * 3;  // CTA i -> axis i % 3
+  // few tiles per CTA: resident weights by one bulk copy (see WBULK)
+  const bool bulk = (tiles + per_axis - 1) / per_axis <= kTcBulkMaxTiles;
+  auto *fn = ctx->tc_stream ? lwpr_tc_kernel<VAR, true>
+                            : (bulk ? lwpr_tc_kernel<VAR, false, true> : lwpr_tc_kernel<VAR, false, false>);
+  TRY(set_smem(ctx, fn, ctx->tc_smem));
   TRY(launch_pdl_if(pdl, ctx, fn, dim3((unsigned)grid), dim3(kTcThreads), ctx->tc_smem, st, a));
   CU(cudaGetLastError());
   return PI2_OK;
