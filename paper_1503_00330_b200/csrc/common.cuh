@@ -16,6 +16,7 @@ constexpr int kLwprBlock = 128;     // threads per LWPR block
 constexpr int kLwprRows = 8;        // rows (k,t) per LWPR thread (register blocking)
 constexpr int kChunk = 256;         // rollouts per leaf partial (fixed => G-invariant tree)
 constexpr int kChunkWarps = 8;      // warps per partials block
+constexpr int kPartialsSplitBlocks = 296;  // below this many partials_kernel blocks, partials_split_kernel
 constexpr int kSeg = 1024;          // leaves per combine segment
 constexpr int kMaxSmallM = 8;       // sub-rollouts held in registers
 constexpr int64_t kWideMaxK = 16384; // up to this K, attitude/rollout use a warp per rollout (latency)

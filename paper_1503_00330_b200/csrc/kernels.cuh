@@ -1111,6 +1111,63 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
   }
 }
 
+// Few (chunk, t) pairs (small K): the same partials with each (chunk, t) spread over
+// a block of kChunk / 32 warps, one element per lane, so the per-element f64 exp and
+// noise regeneration run in parallel rather than as 8 sequential elements per lane.
+// Bitwise equal to partials_kernel: the min is exact in any grouping, and warp 0
+// adds the staged w and w*e in partials_kernel's j order before the same butterfly.
+__global__ void __launch_bounds__(kChunk)
+    partials_split_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
+                          const double *__restrict__ eps, const StepArgs *__restrict__ sa, int iteration,
+                          int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
+  constexpr int J = kChunk / 32;
+  __shared__ double smin[J];
+  __shared__ double sp[J][5][32];  // [j][w, w*e0..w*e3][lane]
+  pdl_wait();
+  const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int t = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t k = k0 + lane + 32 * j;
+  const double s = k < K ? __ldcg(costs + k * cs_k + t * cs_t) : INFINITY;  // coherent (see pdl_wait)
+  double m = warp_min(s);
+  if (lane == 0) smin[j] = m;
+  __syncthreads();
+  m = smin[0];
+#pragma unroll
+  for (int i = 1; i < J; ++i) m = fmin(m, smin[i]);
+  if (k < K) {
+    const double w = exp(__dmul_rn(__dsub_rn(s, m), neg_inv));
+    double e[4];
+    if (eps) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
+      e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    } else {
+      device_eps(sa, iter_key(sa->key_prefix[0], (uint64_t)iteration), (uint64_t)(k_off + k), N, t, e);
+    }
+    sp[j][0][lane] = w;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sp[j][1 + c][lane] = __dmul_rn(w, e[c]);
+  }
+  __syncthreads();
+  if (j != 0) return;
+  double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < J; ++i) {
+    if (k0 + lane + 32 * i >= K) continue;
+    z = __dadd_rn(z, sp[i][0][lane]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __dadd_rn(v[c], sp[i][1 + c][lane]);
+  }
+  z = warp_sum(z);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = warp_sum(v[c]);
+  if (lane == 0) {
+    double *o = out + ((int64_t)blockIdx.x * N + t) * PI2_PARTIAL_WIDTH;
+    o[0] = m; o[1] = z; o[2] = v[0]; o[3] = v[1]; o[4] = v[2]; o[5] = v[3];
+  }
+}
+
 // t-major (N, K) -> reference (K, N), 32x32 tiles through shared memory
 __global__ void transpose_costs_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t K,
                                        int N) {

@@ -54,6 +54,7 @@ struct pi2_ctx {
   bool pdl = true;         // programmatic dependent launch along the step's kernels (PI2_PDL=0: off)
   bool uva = false;        // pinned host memory is device-accessible (unified addressing)
   bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
+  int partials_split = 1;  // partials_split_kernel: 0 never, 1 when few (chunk, t) warps, 2 always
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -498,6 +499,23 @@ dim3 partials_grid(int64_t chunks, int N) {
   return dim3((unsigned)chunks, (unsigned)((N + kChunkWarps - 1) / kChunkWarps));
 }
 
+// leaf partials of `chunks` chunks x N timesteps; the block-per-(chunk, t) kernel when
+// a warp per (chunk, t) would leave most of the GPU idle (same bits either way)
+int launch_partials(pi2_ctx *ctx, const double *costs, int64_t cs_k, int64_t cs_t, const double *eps, int it,
+                    int64_t K, int64_t k_off, int N, double neg_inv, double *out, cudaStream_t st, bool pdl) {
+  const int64_t chunks = (K + kChunk - 1) / kChunk;
+  const dim3 g = partials_grid(chunks, N);
+  const bool split = ctx->partials_split == 2 || (ctx->partials_split == 1 && (int64_t)g.x * g.y < kPartialsSplitBlocks);
+  if (split)
+    TRY(launch_pdl_if(pdl, ctx, partials_split_kernel, dim3((unsigned)chunks, (unsigned)N), dim3(kChunk), 0, st, costs,
+                      cs_k, cs_t, eps, ctx->d_args, it, K, k_off, N, neg_inv, out));
+  else
+    TRY(launch_pdl_if(pdl, ctx, partials_kernel, g, dim3(32 * kChunkWarps), 0, st, costs, cs_k, cs_t, eps,
+                      ctx->d_args, it, K, k_off, N, neg_inv, out));
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
 // after_kernel: the stream predecessor is the partials kernel (PDL allowed);
 // plan_host: also store the updated plan there (see apply_root_kernel)
 int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
@@ -519,10 +537,8 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
                      cudaStream_t st, double *plan_host = nullptr, bool att_pdl = false) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, nullptr, att_pdl));
-  TRY(launch_pdl(ctx, partials_kernel, partials_grid(ctx->n_chunks, ctx->N), dim3(32 * kChunkWarps), 0, st,
-                 ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, it, ctx->K, ctx->dims.rollout_offset, ctx->N,
-                 neg_inv, ctx->d_partials));
-  CU(cudaGetLastError());
+  TRY(launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+                      ctx->d_partials, st, true));
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
                         update_plan ? ctx->d_plan : nullptr, st, true, plan_host);
 }
@@ -608,6 +624,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (const char *e = getenv("PI2_PDL")) ctx->pdl = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_IO_PULL")) ctx->io_pull = std::atoi(e) != 0;
+  if (const char *e = getenv("PI2_PARTIALS_SPLIT")) ctx->partials_split = std::atoi(e);
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
@@ -815,9 +832,7 @@ int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, co
   double *dplan = partials + PI2_PARTIAL_WIDTH * chunks * N;
   CU(cudaMemcpyAsync(dplan, plan, plbytes, cudaMemcpyHostToDevice, st));
   const double neg_inv = -1.0 / temperature;
-  partials_kernel<<<partials_grid(chunks, N), 32 * kChunkWarps, 0, st>>>(costs_dev, N, 1, noise_dev, ctx->d_args,
-                                                                         0, K, 0, N, neg_inv, partials);
-  CU(cudaGetLastError());
+  TRY(launch_partials(ctx, costs_dev, N, 1, noise_dev, 0, K, 0, N, neg_inv, partials, st, false));
   TRY(launch_combine(ctx, partials, chunks, N, neg_inv, nullptr, dplan, st));
   CU(cudaMemcpyAsync(plan_out, dplan, plbytes, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -992,9 +1007,9 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
     rc = launch_rollouts(ctx, 0, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, ev);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[3], st);
-    partials_kernel<<<partials_grid(ctx->n_chunks, ctx->N), 32 * kChunkWarps, 0, st>>>(
-        ctx->d_costs, 1, ctx->K, nullptr, ctx->d_args, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
-        ctx->d_partials);
+    rc = launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+                         ctx->d_partials, st, false);
+    if (rc != PI2_OK) break;
     cudaEventRecord(ev[4], st);
     rc = launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, ctx->d_root, nullptr, st);
     cudaEventRecord(ev[5], st);

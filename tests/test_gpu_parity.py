@@ -454,6 +454,33 @@ def test_programmatic_dependent_launch_is_bitwise_neutral(K, M, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("K,N", [(1000, 20), (3000, 37), (70000, 9)])
+def test_split_partials_kernel_is_bitwise_equal(K, N, monkeypatch):
+    """partials_split_kernel (a block per (chunk, t), used when few (chunk, t) pairs) and
+    partials_kernel (a warp per (chunk, t)) give the same bits: device-noise optimize
+    and the host-noise update path, ragged last chunks included."""
+    stacks = synthetic.hybrid_stacks(24, seed=K)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    task = P.Task.default()
+    plan = P.ControlPlan.hover(params, N)
+    state = P.QuadState.hover(task.spawn)
+    res = {}
+    for split in ("2", "0"):
+        monkeypatch.setenv("PI2_PARTIALS_SPLIT", split)
+        from paper_1503_00330_b200 import controller as PC
+        monkeypatch.setattr(PC, "_UPDATE_CTX", {})  # the update context reads the switch when created
+        cfg = P.PiConfig(num_rollouts=K, sub_rollouts=1, horizon_steps=N, iterations_per_step=3, rng_seed=2)
+        dev = P.RolloutEngine(model, cfg, device=0, noise="device")
+        eng = P.RolloutEngine(model, cfg, device=0)
+        noise = P.sample_noise(cfg, 1, 0)
+        batch = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1))
+        res[split] = [dev.optimize_device(state, plan, P.RolloutCost(task, 1), c).controls for c in range(2)]
+        res[split].append(P.path_integral_update(plan, batch, cfg.temperature).controls)
+    for a, b in zip(res["2"], res["0"]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_sharded_partials_are_gpu_count_invariant():
     """Rank shards evaluated one after another on one GPU (no cross-waiting kernels):
     the fixed-order combine gives the single-context plan bitwise for G = 2 and 4."""
