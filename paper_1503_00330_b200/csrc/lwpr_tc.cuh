@@ -158,6 +158,14 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 #define PI2_TC_T(i)
 #endif
 
+// software-pipelined TMEM loads in the exp loop: 0 never, 1 streamed weights only, 2 always.
+// With resident weights one 8-field batch is shorter than the TMEM load latency and the
+// per-batch wait costs more (L=100 424 -> 452 us); streamed, it gains 1-4 %
+// (profiles/micro/lwpr_tc_ldpipe_b200.txt)
+#ifndef PI2_TC_LDPIPE
+#define PI2_TC_LDPIPE 1
+#endif
+
 #ifndef PI2_TC_POLY_VAR
 #define PI2_TC_POLY_VAR 0   // field pairs (of 4 per 8-field batch) whose 2^x runs on the FMA pipe:
                             // the variance loop slows down with any (1: 436 -> 456 us at L=100), the
@@ -406,6 +414,30 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
       PI2_TC_T(2);
       const float *slv = slv_base + (int64_t)c * kTcChunk;
       const int nb = lc >> 3;  // 8-field batches, two per TMEM wait
+      if constexpr (PI2_TC_LDPIPE == 2 || (PI2_TC_LDPIPE == 1 && STREAM)) {
+      // each batch's TMEM load is in flight while the previous batch computes
+      // (tcgen05.wait::ld waits for all of a thread's loads: load b + 1, compute b, wait)
+      uint32_t la[8], ya[8], lb[8], yb[8];
+      PI2_TMEM_LD8(la, tmem_lane);
+      PI2_TMEM_LD8(ya, tmem_lane + lc);
+      PI2_TMEM_WAIT16(la, ya);
+      for (int b = 0; b < nb; b += 2) {
+        if (b + 1 < nb) {
+          PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
+          PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+        }
+        tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
+        if (b + 1 < nb) {
+          PI2_TMEM_WAIT16(lb, yb);
+          if (b + 2 < nb) {
+            PI2_TMEM_LD8(la, tmem_lane + 8 * b + 16);
+            PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b + 16);
+          }
+          tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+          if (b + 2 < nb) PI2_TMEM_WAIT16(la, ya);
+        }
+      }
+      } else {
       for (int b = 0; b < nb; b += 2) {
         uint32_t la[8], ya[8], lb[8], yb[8];
         PI2_TMEM_LD8(la, tmem_lane + 8 * b);
@@ -418,6 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
         PI2_TMEM_WAIT16(lb, yb);
         tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
         if (b + 1 < nb) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+      }
       }
       woff += (int64_t)2 * (2 * lc * 8);
       PI2_TC_T(3);
