@@ -423,6 +423,39 @@ def test_full_size_baseline_configs_device_path(K, N, L, M):
     assert np.all(du_err(fused.controls, ref_update, plan.controls) < DU_TOL)
 
 
+@pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (16384, 3, 16, 1),
+                                     (16385, 3, 16, 1), (16385, 2, 16, 4), (300, 7, 130, 2)])
+def test_device_path_edge_shapes(K, N, L, M):
+    """The fused device-noise step at edge shapes (one rollout, one step, odd M, both
+    sides of the warp-per-rollout threshold K = 16384, a 130-field model) equals
+    evaluate + update on the materialised device noise, bitwise, and its costs match
+    the oracle."""
+    stacks = synthetic.hybrid_stacks(L, seed=K + N)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=4)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn + np.array([0.03, 0.02, -0.05]))
+    plan, cost = P.ControlPlan.hover(params, N), P.RolloutCost(task, 1)
+    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+    fused = eng.optimize_device(state, plan, cost, cycle_index=2)
+    ctx = eng.context(K, N)
+    eps = np.empty((K, N, 4))
+    ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, cfg.rng_seed, 2, 0, _abi.ptr(cfg.exploration_std), _abi.ptr(eps))
+    dyn = None
+    if M > 1:
+        dyn = np.empty((K, M, N, 3), np.float32)
+        ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, cfg.rng_seed, 2, 0, None, _abi.ptr(dyn))
+    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, eps, cost, dyn)
+    np.testing.assert_array_equal(fused.controls, P.path_integral_update(plan, b, cfg.temperature).controls)
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, eps, RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES),
+                         dyn, M)
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
 def test_graph_replay_matches_eager_and_is_deterministic():
     params, model, cfg, task, state, plan, cost = _device_setup()
     g = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=True)
