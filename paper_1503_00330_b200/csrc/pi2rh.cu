@@ -55,6 +55,7 @@ struct pi2_ctx {
   bool uva = false;        // pinned host memory is device-accessible (unified addressing)
   bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
   int partials_split = 1;  // partials_split_kernel: 0 never, 1 when few (chunk, t) warps, 2 always
+  int64_t wide_max_k = kWideMaxK;  // attitude/rollout use a warp per rollout up to this K (PI2_WIDE_MAX_K)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -371,7 +372,7 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     if (S <= 16) return launch_group_g<16>(ctx, a, fast, st);
     return launch_group_g<32>(ctx, a, fast, st);
   }
-  if (S == 1 && a.K <= kWideMaxK) {  // latency regime: a warp per rollout
+  if (S == 1 && a.K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
     const unsigned grid = (unsigned)((a.K + kWideWarps - 1) / kWideWarps);
     const int smem = kWideWarps * 11 * a.N * (int)sizeof(float);
     if (hybrid && nav) {
@@ -440,7 +441,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   const int N = ctx->N;
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
   const int psmem = 4 * N * (int)sizeof(double);
-  if (K <= kWideMaxK) {  // latency regime: a warp per rollout
+  if (K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
     const unsigned wgrid = (unsigned)((K + kWideWarps - 1) / kWideWarps);
     const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
     if (noise_dev) {
@@ -625,6 +626,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if (const char *e = getenv("PI2_PDL")) ctx->pdl = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_IO_PULL")) ctx->io_pull = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_PARTIALS_SPLIT")) ctx->partials_split = std::atoi(e);
+  if (const char *e = getenv("PI2_WIDE_MAX_K")) ctx->wide_max_k = std::atoll(e);
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);

@@ -74,7 +74,7 @@ def test_evaluate_matches_reference_golden(name):
     assert np.all(du_err(new.controls, z["new_plan"], z["plan"]) < DU_TOL)
 
 
-# K <= 16384 runs the warp-per-rollout (latency) kernels, larger K the
+# K <= 6144 runs the warp-per-rollout (latency) kernels, larger K the
 # thread-per-rollout / lane-per-sub-rollout ones: both are covered.
 @pytest.mark.parametrize("K,N,L,M,full", [(2048, 50, 100, 4, False), (1500, 50, 100, 1, False),
                                           (777, 20, 40, 3, True), (300, 10, 20, 16, False),
@@ -423,11 +423,11 @@ def test_full_size_baseline_configs_device_path(K, N, L, M):
     assert np.all(du_err(fused.controls, ref_update, plan.controls) < DU_TOL)
 
 
-@pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (16384, 3, 16, 1),
-                                     (16385, 3, 16, 1), (16385, 2, 16, 4), (300, 7, 130, 2)])
+@pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (6144, 3, 16, 1),
+                                     (6145, 3, 16, 1), (6145, 2, 16, 4), (300, 7, 130, 2)])
 def test_device_path_edge_shapes(K, N, L, M):
     """The fused device-noise step at edge shapes (one rollout, one step, odd M, both
-    sides of the warp-per-rollout threshold K = 16384, a 130-field model) equals
+    sides of the warp-per-rollout threshold K = 6144, a 130-field model) equals
     evaluate + update on the materialised device noise, bitwise, and its costs match
     the oracle."""
     stacks = synthetic.hybrid_stacks(L, seed=K + N)
@@ -454,6 +454,30 @@ def test_device_path_edge_shapes(K, N, L, M):
                          dyn, M)
     np.testing.assert_array_equal(b.crash_flags, rf)
     assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+
+
+@pytest.mark.parametrize("K,M", [(3000, 1), (3000, 4), (700, 1)])
+def test_warp_and_thread_per_rollout_kernels_are_bitwise_equal(K, M, monkeypatch):
+    """The attitude / rollout kernels with a warp per rollout (small K) and with a thread
+    (lane) per rollout give the same bits (PI2_WIDE_MAX_K forces either): device-noise
+    optimize and host-noise evaluate."""
+    stacks = synthetic.hybrid_stacks(24, seed=K + M)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    task = P.Task.default()
+    plan = P.ControlPlan.hover(params, 30)
+    state = P.QuadState.hover(task.spawn)
+    res = {}
+    for thr in (str(1 << 30), "0"):
+        monkeypatch.setenv("PI2_WIDE_MAX_K", thr)
+        cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=30, iterations_per_step=2, rng_seed=6)
+        noise = P.sample_noise(cfg, 1, 0)
+        dyn = P.sample_dynamics_noise(cfg, 1, 0) if M > 1 else None
+        b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn)
+        dev = P.RolloutEngine(model, cfg, device=0, noise="device").optimize_device(state, plan, P.RolloutCost(task, 1), 1)
+        res[thr] = (b.costs_to_go, b.crash_flags, dev.controls)
+    for x, y in zip(res[str(1 << 30)], res["0"]):
+        np.testing.assert_array_equal(x, y)
 
 
 def test_graph_replay_matches_eager_and_is_deterministic():
