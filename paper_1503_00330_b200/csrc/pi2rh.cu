@@ -56,6 +56,7 @@ struct pi2_ctx {
   bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
   int partials_split = 1;  // partials_split_kernel: 0 never, 1 when few (chunk, t) warps, 2 always
   int64_t wide_max_k = kWideMaxK;  // attitude/rollout use a warp per rollout up to this K (PI2_WIDE_MAX_K)
+  int64_t tc_bulk_max_tiles = kTcBulkMaxTiles;  // WBULK LWPR up to this many tiles per CTA (PI2_TC_BULK_MAX_TILES)
   LwprTcArgs tc{};
   float *d_tc = nullptr;
   size_t tc_cap = 0;
@@ -259,7 +260,7 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   const int64_t per_axis = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles);
   const int64_t grid = per_axis * 3;  // CTA i -> axis i % 3
   // few tiles per CTA: resident weights by one bulk copy (see WBULK)
-  const bool bulk = (tiles + per_axis - 1) / per_axis <= kTcBulkMaxTiles;
+  const bool bulk = (tiles + per_axis - 1) / per_axis <= ctx->tc_bulk_max_tiles;
   auto *fn = ctx->tc_stream ? lwpr_tc_kernel<VAR, true>
                             : (bulk ? lwpr_tc_kernel<VAR, false, true> : lwpr_tc_kernel<VAR, false, false>);
   TRY(set_smem(ctx, fn, ctx->tc_smem));
@@ -627,6 +628,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if (const char *e = getenv("PI2_IO_PULL")) ctx->io_pull = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_PARTIALS_SPLIT")) ctx->partials_split = std::atoi(e);
   if (const char *e = getenv("PI2_WIDE_MAX_K")) ctx->wide_max_k = std::atoll(e);
+  if (const char *e = getenv("PI2_TC_BULK_MAX_TILES")) ctx->tc_bulk_max_tiles = std::atoll(e);
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
