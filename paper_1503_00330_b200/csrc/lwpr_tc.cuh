@@ -26,6 +26,7 @@
 // this kernel's per-chunk synchronisation.
 #pragma once
 
+#include <type_traits>
 #include <vector>
 
 #include "fold.h"
@@ -164,6 +165,12 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 // (profiles/micro/lwpr_tc_ldpipe_b200.txt)
 #ifndef PI2_TC_LDPIPE
 #define PI2_TC_LDPIPE 1
+#endif
+// full field chunks: the exp loop fully unrolled (compile-time batch count).  Harness,
+// L=100 / 200 variance 426 -> 411 / 746 -> 705 us; unrolling every remainder count as
+// well (8 instantiations) was slower again (profiles/micro/lwpr_tc_unroll_b200.txt)
+#ifndef PI2_TC_UNROLL
+#define PI2_TC_UNROLL 1
 #endif
 
 #ifndef PI2_TC_POLY_VAR
@@ -438,19 +445,31 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
         }
       }
       } else {
-      for (int b = 0; b < nb; b += 2) {
-        uint32_t la[8], ya[8], lb[8], yb[8];
-        PI2_TMEM_LD8(la, tmem_lane + 8 * b);
-        PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b);
-        if (b + 1 < nb) {
-          PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
-          PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+      auto batches = [&](auto nb_c) {  // nb_c: compile-time batch count, or 0 = runtime nb
+        constexpr int NBC = decltype(nb_c)::value;
+        const int n = NBC > 0 ? NBC : nb;
+#pragma unroll
+        for (int b = 0; b < (NBC > 0 ? NBC : 1 << 30); b += 2) {
+          if (NBC == 0 && b >= n) break;
+          uint32_t la[8], ya[8], lb[8], yb[8];
+          PI2_TMEM_LD8(la, tmem_lane + 8 * b);
+          PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b);
+          if (b + 1 < n) {
+            PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
+            PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+          }
+          PI2_TMEM_WAIT16(la, ya);
+          PI2_TMEM_WAIT16(lb, yb);
+          tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
+          if (b + 1 < n) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
         }
-        PI2_TMEM_WAIT16(la, ya);
-        PI2_TMEM_WAIT16(lb, yb);
-        tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
-        if (b + 1 < nb) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
-      }
+      };
+#if PI2_TC_UNROLL
+      if (lc == kTcChunk) batches(std::integral_constant<int, kTcChunk / 8>{});
+      else batches(std::integral_constant<int, 0>{});
+#else
+      batches(std::integral_constant<int, 0>{});
+#endif
       }
       woff += (int64_t)2 * (2 * lc * 8);
       PI2_TC_T(3);
