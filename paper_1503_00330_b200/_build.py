@@ -56,7 +56,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     tmp = OUT + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, os.path.join(CSRC, "pi2rh.cu")]
+    # PI2_NVCC_EXTRA: extra flags for experiments (e.g. "-DPI2_ROLL_UNROLL=2"); not used by default
+    extra = os.environ.get("PI2_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, os.path.join(CSRC, "pi2rh.cu")]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -565,6 +565,11 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
   return __fadd_rn(out, crashed ? 10.0f : 0.0f);
 }
 
+#ifndef PI2_ROLL1_UNROLL
+#define PI2_ROLL1_UNROLL 1  // t-loop unroll of rollout_kernel
+#endif
+constexpr int kRoll1Unroll = PI2_ROLL1_UNROLL;
+
 // MM: compile-time sub-rollouts held in registers (1), or 0 = runtime M <= PI2_MAX_SUB_ROLLOUTS.
 // FAST: hybrid LWPR model + navigation cost, branches folded at compile time.
 template <int MM, bool FAST>
@@ -610,6 +615,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, k);
   float4 apn = (1 < N) ? __ldg(a.xin + a.K + k) : __ldg(a.ang_last + k);
   float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll(kRoll1Unroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
     const float3 m4 = m4n, s4 = s4n;
@@ -727,6 +733,11 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   a.crash[k] = crash ? 1 : 0;
 }
 
+#ifndef PI2_ROLL_UNROLL
+#define PI2_ROLL_UNROLL 4  // t-loop unroll of rollout_group_kernel (C2 0.633 -> 0.629 ms, micro/roll_unroll_b200.txt)
+#endif
+constexpr int kRollUnroll = PI2_ROLL_UNROLL;
+
 // Sub-rollouts on lanes: a group of G lanes (G = S rounded up to a power of
 // two, <= 32) per rollout, lane m integrating sub-rollout m.  The M-mean is
 // the reference's pairwise tree (controller.py:314-319): for S == G an xor
@@ -779,6 +790,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
     }
     apn = (1 < N) ? __ldg(a.xin + a.K + kk) : __ldg(a.ang_last + kk);
   }
+#pragma unroll(kRollUnroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + kk;
     const float3 m4 = m4n, s4 = s4n;
