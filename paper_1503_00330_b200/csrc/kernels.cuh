@@ -109,6 +109,14 @@ __device__ __forceinline__ double wrap_angle(double a) {
 // K1-K3: u = clip(plan + eps), attitude recurrence, LWPR input rows.
 // controller.py:257-275.  One thread per rollout, FP64, no contraction.
 // ---------------------------------------------------------------------------
+#ifndef PI2_ATT_TB
+#define PI2_ATT_TB 4
+#endif
+#ifndef PI2_ATT_UNROLL
+#define PI2_ATT_UNROLL 1
+#endif
+constexpr int kAttUnroll = PI2_ATT_UNROLL;
+
 template <bool DEVICE_NOISE>
 __global__ void __launch_bounds__(kRolloutBlock)
     attitude_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
@@ -127,7 +135,8 @@ __global__ void __launch_bounds__(kRolloutBlock)
   const double *ek = DEVICE_NOISE ? nullptr : eps + k * (int64_t)N * 4;
   const Key128 ck = DEVICE_NOISE ? iter_key(sa->key_prefix[0], (uint64_t)iteration) : Key128{0, 0};
   float4 *xk = xin + k;  // row (k, t) at xk[t * K]
-  constexpr int TB = 4;  // noise of TB steps is generated before their serial FP64 recurrence
+  constexpr int TB = PI2_ATT_TB;  // noise of TB steps is generated before their serial FP64 recurrence
+#pragma unroll(kAttUnroll)
   for (int t0 = 0; t0 < N; t0 += TB) {
     double e[TB][4];
 #pragma unroll
