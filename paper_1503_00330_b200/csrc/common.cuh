@@ -11,7 +11,10 @@
 
 namespace pi2 {
 
-constexpr int kRolloutBlock = 128;  // threads (= rollouts) per attitude / rollout block
+#ifndef PI2_ROLL_BLOCK
+#define PI2_ROLL_BLOCK 128
+#endif
+constexpr int kRolloutBlock = PI2_ROLL_BLOCK;  // threads (= rollouts) per attitude / rollout block
 constexpr int kLwprBlock = 128;     // threads per LWPR block
 constexpr int kLwprRows = 8;        // rows (k,t) per LWPR thread (register blocking)
 constexpr int kChunk = 256;         // rollouts per leaf partial (fixed => G-invariant tree)
