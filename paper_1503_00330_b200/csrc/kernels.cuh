@@ -70,13 +70,18 @@ __device__ __forceinline__ float4 normals4(uint64_t index, uint64_t k0, uint64_t
 
 // exploration noise eps[k, t, :] of the device stream (float32 normals x float64 std)
 // (key: iter_key(sa->key_prefix[0], iteration), derived once per thread)
-__device__ __forceinline__ void device_eps(const StepArgs *sa, Key128 key, uint64_t kg, int N, int t,
-                                           double e[4]) {
-  const float4 z = normals4(kg * (uint64_t)N + (uint64_t)t, key.k0, key.k1);
+__device__ __forceinline__ void eps_from_z(const StepArgs *sa, float4 z, double e[4]) {
   e[0] = __dmul_rn((double)z.x, sa->std[0]);
   e[1] = __dmul_rn((double)z.y, sa->std[1]);
   e[2] = __dmul_rn((double)z.z, sa->std[2]);
   e[3] = __dmul_rn((double)z.w, sa->std[3]);
+}
+__device__ __forceinline__ float4 device_z(Key128 key, uint64_t kg, int N, int t) {
+  return normals4(kg * (uint64_t)N + (uint64_t)t, key.k0, key.k1);
+}
+__device__ __forceinline__ void device_eps(const StepArgs *sa, Key128 key, uint64_t kg, int N, int t,
+                                           double e[4]) {
+  eps_from_z(sa, device_z(key, kg, N, t), e);
 }
 
 // np.clip(v, lo, hi, out=...) with array bounds (controller.py:259, :371): numpy's
@@ -122,7 +127,9 @@ __global__ void __launch_bounds__(kRolloutBlock)
     attitude_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
                     const double *__restrict__ eps, int iteration, int64_t K, int64_t k_off, int N,
                     DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last,
-                    double *__restrict__ eps_out) {
+                    float4 *__restrict__ zout) {
+  // zout (device noise): the exploration normals z(k, t) at zout[t * K + k] for the
+  // partials kernel, which would otherwise regenerate them (e = z * std either way)
   extern __shared__ double splan[];  // (N, 4)
   pdl_wait();     // the plan is the previous iteration's update
   pdl_trigger();  // one wave: the LWPR kernel's prologue may start on free SM resources
@@ -143,7 +150,9 @@ __global__ void __launch_bounds__(kRolloutBlock)
     for (int j = 0; j < TB; ++j) {
       const int t = t0 + j < N ? t0 + j : N - 1;
       if (DEVICE_NOISE) {
-        device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e[j]);
+        const float4 z = device_z(ck, (uint64_t)(k_off + k), N, t);
+        if (zout && t0 + j < N) zout[(int64_t)t * K + k] = z;
+        eps_from_z(sa, z, e[j]);
       } else {
         const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
         const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
@@ -154,11 +163,6 @@ __global__ void __launch_bounds__(kRolloutBlock)
     for (int j = 0; j < TB; ++j) {
       const int t = t0 + j;
       if (t >= N) break;
-      if (DEVICE_NOISE && eps_out) {
-        double2 *o = reinterpret_cast<double2 *>(eps_out + (k * (int64_t)N + t) * 4);
-        o[0] = make_double2(e[j][0], e[j][1]);
-        o[1] = make_double2(e[j][2], e[j][3]);
-      }
       double u[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -926,7 +930,8 @@ template <bool DEVICE_NOISE>
 __global__ void __launch_bounds__(32 * kWideWarps)
     attitude_wide_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
                          const double *__restrict__ eps, int iteration, int64_t K, int64_t k_off, int N,
-                         DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last) {
+                         DynParams dp, float4 *__restrict__ xin, float4 *__restrict__ ang_last,
+                         float4 *__restrict__ zout) {
   extern __shared__ double wsm[];
   double *splan = wsm;                                   // (N, 4)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -942,7 +947,9 @@ __global__ void __launch_bounds__(32 * kWideWarps)
   for (int t = lane; t < N; t += 32) {
     double e[4];
     if (DEVICE_NOISE) {
-      device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e);
+      const float4 z = device_z(ck, (uint64_t)(k_off + k), N, t);
+      if (zout) zout[(int64_t)t * K + k] = z;
+      eps_from_z(sa, z, e);
     } else {
       const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
       const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
@@ -1087,7 +1094,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __global__ void __launch_bounds__(32 * kChunkWarps)
     partials_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
-                    const double *__restrict__ eps, const StepArgs *__restrict__ sa, int iteration,
+                    const double *__restrict__ eps, const float4 *zin, const StepArgs *__restrict__ sa, int iteration,
                     int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
   constexpr int J = kChunk / 32;
   pdl_wait();
@@ -1105,7 +1112,7 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
   }
   m = warp_min(m);
   double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
-  const Key128 ck = eps ? Key128{0, 0} : iter_key(sa->key_prefix[0], (uint64_t)iteration);
+  const Key128 ck = (eps || zin) ? Key128{0, 0} : iter_key(sa->key_prefix[0], (uint64_t)iteration);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int64_t k = k0 + lane + 32 * j;
@@ -1116,6 +1123,8 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
       const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
       const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
       e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    } else if (zin) {  // the attitude kernel's normals (coherent: written earlier in the chain)
+      eps_from_z(sa, __ldcg(zin + (int64_t)t * K + k), e);
     } else {
       device_eps(sa, ck, (uint64_t)(k_off + k), N, t, e);
     }
@@ -1139,7 +1148,8 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
 // adds the staged w and w*e in partials_kernel's j order before the same butterfly.
 __global__ void __launch_bounds__(kChunk)
     partials_split_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
-                          const double *__restrict__ eps, const StepArgs *__restrict__ sa, int iteration,
+                          const double *__restrict__ eps, const float4 *zin, const StepArgs *__restrict__ sa,
+                          int iteration,
                           int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
   constexpr int J = kChunk / 32;
   __shared__ double smin[J];
@@ -1163,6 +1173,8 @@ __global__ void __launch_bounds__(kChunk)
       const double2 a = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4));
       const double2 b = __ldg(reinterpret_cast<const double2 *>(eps + (k * N + t) * 4) + 1);
       e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+    } else if (zin) {
+      eps_from_z(sa, __ldcg(zin + (int64_t)t * K + k), e);
     } else {
       device_eps(sa, iter_key(sa->key_prefix[0], (uint64_t)iteration), (uint64_t)(k_off + k), N, t, e);
     }

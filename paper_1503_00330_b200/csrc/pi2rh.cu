@@ -71,6 +71,7 @@ struct pi2_ctx {
   double *d_costs = nullptr;
   uint8_t *d_crash = nullptr;
   double *d_partials = nullptr, *d_root = nullptr;
+  float4 *d_z = nullptr;  // device-noise exploration normals z(k, t) at [t * K + k] (attitude -> partials)
   int64_t n_chunks = 0;
   // lazily grown scratch
   double *d_noise = nullptr;
@@ -449,12 +450,12 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
       TRY(set_smem(ctx, attitude_wide_kernel<false>, wsmem));
       TRY(launch_pdl_if(att_pdl, ctx, attitude_wide_kernel<false>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
                      ctx->d_plan, noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
-                     ctx->d_ang_last));
+                     ctx->d_ang_last, nullptr));
     } else {
       TRY(set_smem(ctx, attitude_wide_kernel<true>, wsmem));
       TRY(launch_pdl_if(att_pdl, ctx, attitude_wide_kernel<true>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
                      ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
-                     ctx->d_ang_last));
+                     ctx->d_ang_last, ctx->d_z));
     }
   } else if (noise_dev) {
     TRY(set_smem(ctx, attitude_kernel<false>, psmem));
@@ -464,7 +465,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   } else {
     TRY(set_smem(ctx, attitude_kernel<true>, psmem));
     TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
-                   nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, nullptr));
+                   nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, ctx->d_z));
   }
   CU(cudaGetLastError());
   if (ev) CU(cudaEventRecord(ev[1], st));
@@ -503,16 +504,19 @@ dim3 partials_grid(int64_t chunks, int N) {
 
 // leaf partials of `chunks` chunks x N timesteps; the block-per-(chunk, t) kernel when
 // a warp per (chunk, t) would leave most of the GPU idle (same bits either way)
-int launch_partials(pi2_ctx *ctx, const double *costs, int64_t cs_k, int64_t cs_t, const double *eps, int it,
-                    int64_t K, int64_t k_off, int N, double neg_inv, double *out, cudaStream_t st, bool pdl) {
+// zin: the device-noise normals the attitude kernel stored (ctx->d_z); nullptr with host
+// noise (eps)
+int launch_partials(pi2_ctx *ctx, const double *costs, int64_t cs_k, int64_t cs_t, const double *eps,
+                    const float4 *zin, int it, int64_t K, int64_t k_off, int N, double neg_inv, double *out,
+                    cudaStream_t st, bool pdl) {
   const int64_t chunks = (K + kChunk - 1) / kChunk;
   const dim3 g = partials_grid(chunks, N);
   const bool split = ctx->partials_split == 2 || (ctx->partials_split == 1 && (int64_t)g.x * g.y < kPartialsSplitBlocks);
   if (split)
     TRY(launch_pdl_if(pdl, ctx, partials_split_kernel, dim3((unsigned)chunks, (unsigned)N), dim3(kChunk), 0, st, costs,
-                      cs_k, cs_t, eps, ctx->d_args, it, K, k_off, N, neg_inv, out));
+                      cs_k, cs_t, eps, zin, ctx->d_args, it, K, k_off, N, neg_inv, out));
   else
-    TRY(launch_pdl_if(pdl, ctx, partials_kernel, g, dim3(32 * kChunkWarps), 0, st, costs, cs_k, cs_t, eps,
+    TRY(launch_pdl_if(pdl, ctx, partials_kernel, g, dim3(32 * kChunkWarps), 0, st, costs, cs_k, cs_t, eps, zin,
                       ctx->d_args, it, K, k_off, N, neg_inv, out));
   CU(cudaGetLastError());
   return PI2_OK;
@@ -539,7 +543,7 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
                      cudaStream_t st, double *plan_host = nullptr, bool att_pdl = false) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, nullptr, att_pdl));
-  TRY(launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+  TRY(launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->d_z, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
                       ctx->d_partials, st, true));
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
                         update_plan ? ctx->d_plan : nullptr, st, true, plan_host);
@@ -657,6 +661,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   ALLOC(ctx->d_crash, K);
   ALLOC(ctx->d_partials, sizeof(double) * PI2_PARTIAL_WIDTH * ctx->n_chunks * N);
   ALLOC(ctx->d_root, sizeof(double) * PI2_PARTIAL_WIDTH * N);
+  ALLOC(ctx->d_z, sizeof(float4) * K * N);
 #undef ALLOC
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming) != cudaSuccess ||
@@ -682,7 +687,7 @@ void pi2_destroy(pi2_ctx *ctx) {
   invalidate_graph(ctx);
   void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_io,     ctx->d_plan2,    ctx->d_xin,
                   ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
-                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch};
+                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch, ctx->d_z};
   for (void *p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_io) cudaFreeHost(ctx->h_io);
@@ -836,7 +841,7 @@ int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, co
   double *dplan = partials + PI2_PARTIAL_WIDTH * chunks * N;
   CU(cudaMemcpyAsync(dplan, plan, plbytes, cudaMemcpyHostToDevice, st));
   const double neg_inv = -1.0 / temperature;
-  TRY(launch_partials(ctx, costs_dev, N, 1, noise_dev, 0, K, 0, N, neg_inv, partials, st, false));
+  TRY(launch_partials(ctx, costs_dev, N, 1, noise_dev, nullptr, 0, K, 0, N, neg_inv, partials, st, false));
   TRY(launch_combine(ctx, partials, chunks, N, neg_inv, nullptr, dplan, st));
   CU(cudaMemcpyAsync(plan_out, dplan, plbytes, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -1011,7 +1016,7 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
     rc = launch_rollouts(ctx, 0, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, ev);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[3], st);
-    rc = launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+    rc = launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->d_z, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
                          ctx->d_partials, st, false);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[4], st);
