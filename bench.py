@@ -432,7 +432,8 @@ def run_ours(args, rank: int, world: int, local: int):
                                                     if world > 1 and args.scaling == "weak" else ""),
             "K": K, "K_per_gpu": k_local, "T": T, "L": L, "M": M, "iterations_per_step": 1,
             "parallelism": f"rollouts sharded over {world} GPU(s)",
-            "l2": "working set > L2 (xin+LWPR rows+costs ≈ %.0f MB per GPU)" % ((k_local * T * (16 + 32 + 8)) / 1e6),
+            "l2": "working set > L2 (xin + LWPR planes + exploration normals + costs ≈ %.0f MB per GPU)"
+                  % ((k_local * T * (16 + 24 + 16 + 8)) / 1e6),
         },
         "e2e": {
             "value": K * T * args.steps / e2e_s,
