@@ -92,23 +92,6 @@ __device__ __forceinline__ double clip_np(double v, double lo, double hi) {
   return (t < hi || t != t) ? t : hi;
 }
 
-// wrap_angle: pi - mod(pi - a, 2 pi) with numpy float remainder semantics
-// (dynamics.py:27-29; npy_divmod: fmod, then shift into the divisor's sign).
-__device__ __forceinline__ double wrap_angle(double a) {
-  const double x = __dsub_rn(kPi, a);
-  // fmod(x, 2pi) is x for |x| < 2pi and the exact x - 2pi on [2pi, 4pi]
-  // (Sterbenz); anything else takes the general (exact) fmod.
-  double m;
-  if (x > -kTwoPi && x < kTwoPi) m = x;
-  else if (x >= kTwoPi && x <= 2.0 * kTwoPi) m = __dsub_rn(x, kTwoPi);
-  else m = fmod(x, kTwoPi);
-  if (m != 0.0) {
-    if (m < 0.0) m = __dadd_rn(m, kTwoPi);
-  } else {
-    m = 0.0;
-  }
-  return __dsub_rn(kPi, m);
-}
 
 // ---------------------------------------------------------------------------
 // K1-K3: u = clip(plan + eps), attitude recurrence, LWPR input rows.
@@ -962,11 +945,13 @@ __global__ void __launch_bounds__(32 * kWideWarps)
   __syncwarp();
   if (lane < 3) {
     const int c = lane;
+    const double dt = dp.dt, gdt = dp.gain_dt;
     double ang = sa->state[6 + c], rate = sa->state[9 + c];
-    for (int t = 0; t < N; ++t) {
+#pragma unroll 4
+    for (int t = 0; t < N; ++t) {  // the serial chain: controls prefetched from shared memory by the unroll
       reinterpret_cast<float *>(&stage[t])[c] = __double2float_rn(ang);
-      ang = wrap_angle(__dadd_rn(ang, __dmul_rn(rate, dp.dt)));
-      rate = __dadd_rn(rate, __dmul_rn(dp.gain_dt, __dsub_rn(u[4 * t + c], rate)));
+      ang = wrap_angle(__dadd_rn(ang, __dmul_rn(rate, dt)));
+      rate = __dadd_rn(rate, __dmul_rn(gdt, __dsub_rn(u[4 * t + c], rate)));
     }
     reinterpret_cast<float *>(&stage[N])[c] = __double2float_rn(ang);
   }
