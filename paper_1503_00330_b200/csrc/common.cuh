@@ -11,7 +11,7 @@
 
 namespace pi2 {
 
-#ifndef PI2_ROLL_BLOCK
+#ifndef PI2_ROLL_BLOCK  // threads per attitude / rollout block (micro/roll_block_b200.txt: 64 = 128 < 256)
 #define PI2_ROLL_BLOCK 128
 #endif
 constexpr int kRolloutBlock = PI2_ROLL_BLOCK;  // threads (= rollouts) per attitude / rollout block

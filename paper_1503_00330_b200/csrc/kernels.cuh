@@ -97,6 +97,8 @@ __device__ __forceinline__ double clip_np(double v, double lo, double hi) {
 // K1-K3: u = clip(plan + eps), attitude recurrence, LWPR input rows.
 // controller.py:257-275.  One thread per rollout, FP64, no contraction.
 // ---------------------------------------------------------------------------
+// attitude_kernel: device noise of PI2_ATT_TB steps is generated ahead of their serial
+// FP64 recurrence; PI2_ATT_UNROLL unrolls the outer loop (micro/att_tune_b200.txt: 4 / 1)
 #ifndef PI2_ATT_TB
 #define PI2_ATT_TB 4
 #endif
@@ -562,7 +564,7 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
 }
 
 #ifndef PI2_ROLL1_UNROLL
-#define PI2_ROLL1_UNROLL 1  // t-loop unroll of rollout_kernel
+#define PI2_ROLL1_UNROLL 1  // t-loop unroll of rollout_kernel (2 / 4 within noise at C4: micro/roll_unroll_b200.txt)
 #endif
 constexpr int kRoll1Unroll = PI2_ROLL1_UNROLL;
 
