@@ -135,6 +135,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
                  "=r"((r)[6]), "=r"((r)[7])                                                            \
                : "r"(addr))
 
+#define PI2_TMEM_LD16(r, addr)                                                                     \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"((r)[0]), "=r"((r)[1]), "=r"((r)[2]), "=r"((r)[3]), "=r"((r)[4]), "=r"((r)[5]), \
+                 "=r"((r)[6]), "=r"((r)[7]), "=r"((r)[8]), "=r"((r)[9]), "=r"((r)[10]), "=r"((r)[11]), \
+                 "=r"((r)[12]), "=r"((r)[13]), "=r"((r)[14]), "=r"((r)[15])                          \
+               : "r"(addr))
+
 #define PI2_TMEM_WAIT16(a, b)                                                                      \
   asm volatile("tcgen05.wait::ld.sync.aligned;"                                                   \
                : "+r"((a)[0]), "+r"((a)[1]), "+r"((a)[2]), "+r"((a)[3]), "+r"((a)[4]), "+r"((a)[5]),  \
@@ -171,6 +178,9 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 // well (8 instantiations) was slower again (profiles/micro/lwpr_tc_unroll_b200.txt)
 #ifndef PI2_TC_UNROLL
 #define PI2_TC_UNROLL 1
+#endif
+#ifndef PI2_TC_LD16  // 16-column tcgen05.ld in the unrolled full-chunk loop (variance kernels)
+#define PI2_TC_LD16 1
 #endif
 
 #ifndef PI2_TC_POLY_VAR
@@ -448,6 +458,23 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
       auto batches = [&](auto nb_c) {  // nb_c: compile-time batch count, or 0 = runtime nb
         constexpr int NBC = decltype(nb_c)::value;
         const int n = NBC > 0 ? NBC : nb;
+#if PI2_TC_LD16
+        // 16-column TMEM loads, one per operand per batch pair: variance loop only (harness L=100
+        // 411 -> 406 us, L=200 704 -> 692 us); the mean-only loop spills with them and loses 4-5 %
+        if constexpr (VAR && NBC > 0 && NBC % 2 == 0) {
+#pragma unroll
+          for (int b = 0; b < NBC; b += 2) {
+            uint32_t l16[16], y16[16];
+            PI2_TMEM_LD16(l16, tmem_lane + 8 * b);
+            PI2_TMEM_LD16(y16, tmem_lane + lc + 8 * b);
+            PI2_TMEM_WAIT16(l16, y16);
+            PI2_TMEM_WAIT16(l16 + 8, y16 + 8);
+            tc_fields8<VAR>(l16, y16, slv + 8 * b, den, num, m2, lv);
+            tc_fields8<VAR, true>(l16 + 8, y16 + 8, slv + 8 * b + 8, den, num, m2, lv);
+          }
+          return;
+        }
+#endif
 #pragma unroll
         for (int b = 0; b < (NBC > 0 ? NBC : 1 << 30); b += 2) {
           if (NBC == 0 && b >= n) break;
