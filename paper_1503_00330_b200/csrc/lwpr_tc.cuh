@@ -166,12 +166,12 @@ __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barri
 #define PI2_TC_T(i)
 #endif
 
-// software-pipelined TMEM loads in the exp loop: 0 never, 1 streamed weights only, 2 always.
-// With resident weights one 8-field batch is shorter than the TMEM load latency and the
-// per-batch wait costs more (L=100 424 -> 452 us); streamed, it gains 1-4 %
-// (profiles/micro/lwpr_tc_ldpipe_b200.txt)
+// software-pipelined TMEM loads in the exp loop (runtime batch loop): 0 never, 1 streamed
+// weights only, 2 always.  Against the runtime loop it won for streamed weights (C3 25.3 ->
+// 24.3 ms); the unrolled full-chunk loop (PI2_TC_UNROLL) beats both (streamed L=1000
+// variance 3733 -> 3163 us, mean-only 2955 -> 2714 us: micro/lwpr_tc_stream_unroll_b200.txt)
 #ifndef PI2_TC_LDPIPE
-#define PI2_TC_LDPIPE 1
+#define PI2_TC_LDPIPE 0
 #endif
 // full field chunks: the exp loop fully unrolled (compile-time batch count).  Harness,
 // L=100 / 200 variance 426 -> 411 / 746 -> 705 us; unrolling every remainder count as
