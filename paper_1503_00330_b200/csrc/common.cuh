@@ -22,8 +22,8 @@ constexpr int kChunkWarps = 8;      // warps per partials block
 constexpr int kPartialsSplitBlocks = 296;  // below this many partials_kernel blocks, partials_split_kernel
 constexpr int kSeg = 1024;          // leaves per combine segment
 constexpr int kMaxSmallM = 8;       // sub-rollouts held in registers
-constexpr int64_t kWideMaxK = 6144;  // up to this K, attitude/rollout use a warp per rollout (latency);
-                                     // measured crossover ~6656 (profiles/micro/wide_threshold_b200.txt)
+constexpr int64_t kWideMaxK = 8192;  // up to this K, attitude/rollout use a warp per rollout (latency);
+                                     // measured crossover ~8192 (profiles/micro/wide_threshold_b200.txt)
 constexpr double kPi = 3.141592653589793;        // np.pi
 constexpr double kTwoPi = 6.283185307179586;     // 2.0 * math.pi
 constexpr double kLog2e = 1.4426950408889634;

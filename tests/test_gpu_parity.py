@@ -74,7 +74,7 @@ def test_evaluate_matches_reference_golden(name):
     assert np.all(du_err(new.controls, z["new_plan"], z["plan"]) < DU_TOL)
 
 
-# K <= 6144 runs the warp-per-rollout (latency) kernels, larger K the
+# K <= 8192 runs the warp-per-rollout (latency) kernels, larger K the
 # thread-per-rollout / lane-per-sub-rollout ones: both are covered.
 @pytest.mark.parametrize("K,N,L,M,full", [(2048, 50, 100, 4, False), (1500, 50, 100, 1, False),
                                           (777, 20, 40, 3, True), (300, 10, 20, 16, False),
@@ -423,11 +423,11 @@ def test_full_size_baseline_configs_device_path(K, N, L, M):
     assert np.all(du_err(fused.controls, ref_update, plan.controls) < DU_TOL)
 
 
-@pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (6144, 3, 16, 1),
-                                     (6145, 3, 16, 1), (6145, 2, 16, 4), (300, 7, 130, 2)])
+@pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (8192, 3, 16, 1),
+                                     (8193, 3, 16, 1), (8193, 2, 16, 4), (300, 7, 130, 2)])
 def test_device_path_edge_shapes(K, N, L, M):
     """The fused device-noise step at edge shapes (one rollout, one step, odd M, both
-    sides of the warp-per-rollout threshold K = 6144, a 130-field model) equals
+    sides of the warp-per-rollout threshold K = 8192, a 130-field model) equals
     evaluate + update on the materialised device noise, bitwise, and its costs match
     the oracle."""
     stacks = synthetic.hybrid_stacks(L, seed=K + N)
