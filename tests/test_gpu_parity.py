@@ -480,6 +480,40 @@ def test_warp_and_thread_per_rollout_kernels_are_bitwise_equal(K, M, monkeypatch
         np.testing.assert_array_equal(x, y)
 
 
+def test_io_pull_kernel_and_copy_node_give_the_same_step(monkeypatch):
+    """The real-time graph's inputs arrive by io_pull_kernel (default) or by a copy-engine
+    node (PI2_IO_PULL=0): the same controls and plans, bit for bit, over a receding loop."""
+    params, model, cfg, task, state, plan, cost = _device_setup(K=2000, N=30)
+    res = {}
+    for pull in ("1", "0"):
+        monkeypatch.setenv("PI2_IO_PULL", pull)
+        eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+        p, out = plan, []
+        for c in range(4):
+            ctrl, p = P.receding_horizon_step(state, p, cfg, model, cost, c, eng)
+            out += [ctrl.as_array(), p.controls.copy()]
+        res[pull] = out
+    for a, b in zip(res["1"], res["0"]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_profile_iteration_reports_stages_and_leaves_the_plan():
+    """pi2_profile_iteration (bench.py's per-kernel timing) returns positive stage times
+    and does not change the device-resident plan."""
+    params, model, cfg, task, state, plan, cost = _device_setup(K=3000, N=30)
+    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+    P.receding_horizon_step(state, plan, cfg, model, cost, 0, eng)  # binds dynamics and cost
+    ctx = eng.context(cfg.num_rollouts, cfg.horizon_steps)
+    from paper_1503_00330_b200.controller import optimize_args
+    ctx.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan.controls)), None)
+    stages = (_abi.C.c_double * 5)()
+    ctx.call("pi2_profile_iteration", optimize_args(cfg, 0, use_graph=False), 3, stages)
+    assert all(v > 0 for v in stages), list(stages)
+    back = np.empty((cfg.horizon_steps, 4))
+    ctx.call("pi2_read_plan", _abi.ptr(back), None)
+    np.testing.assert_array_equal(back, plan.controls)
+
+
 def test_graph_replay_matches_eager_and_is_deterministic():
     params, model, cfg, task, state, plan, cost = _device_setup()
     g = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=True)
