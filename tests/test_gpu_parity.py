@@ -514,6 +514,32 @@ def test_profile_iteration_reports_stages_and_leaves_the_plan():
     np.testing.assert_array_equal(back, plan.controls)
 
 
+@pytest.mark.parametrize("L,M", [(48, 4), (100, 1), (130, 2)])
+def test_streamed_and_resident_lwpr_weights_are_bitwise_equal(L, M, monkeypatch):
+    """The tensor-core LWPR kernel with its weights TMA-streamed per chunk
+    (PI2_LWPR_TC_STREAM=1) and resident in shared memory (default where they fit) does the
+    same arithmetic: identical costs and updates."""
+    stacks = synthetic.hybrid_stacks(L, seed=L)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    task = P.Task.default()
+    cfg = P.PiConfig(num_rollouts=20000, sub_rollouts=M, horizon_steps=12, iterations_per_step=1, rng_seed=8)
+    state, plan, cost = P.QuadState.hover(task.spawn), P.ControlPlan.hover(params, 12), P.RolloutCost(task, 1)
+    res = {}
+    for stream in ("1", None):
+        if stream:
+            monkeypatch.setenv("PI2_LWPR_TC_STREAM", stream)
+        else:
+            monkeypatch.delenv("PI2_LWPR_TC_STREAM", raising=False)
+        noise = P.sample_noise(cfg, 1, 0)
+        dyn = P.sample_dynamics_noise(cfg, 1, 0) if M > 1 else None
+        b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, noise, cost, dyn)
+        dev = P.RolloutEngine(model, cfg, device=0, noise="device").optimize_device(state, plan, cost, 2)
+        res[stream] = (b.costs_to_go, dev.controls)
+    for a, b in zip(res["1"], res[None]):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_graph_replay_matches_eager_and_is_deterministic():
     params, model, cfg, task, state, plan, cost = _device_setup()
     g = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=True)
