@@ -540,6 +540,23 @@ def test_streamed_and_resident_lwpr_weights_are_bitwise_equal(L, M, monkeypatch)
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("K", [1024, 20000])
+def test_bulk_copy_and_ldg_weight_prologues_are_bitwise_equal(K, monkeypatch):
+    """The resident-weight prologue by one TMA bulk copy (WBULK, few tiles per CTA) and by
+    the LDG/STS loop load the same bytes: identical device-path updates either way."""
+    stacks = synthetic.hybrid_stacks(64, seed=K)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    task = P.Task.default()
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=2, horizon_steps=16, iterations_per_step=2, rng_seed=9)
+    state, plan, cost = P.QuadState.hover(task.spawn), P.ControlPlan.hover(params, 16), P.RolloutCost(task, 1)
+    res = {}
+    for tiles in ("0", "1000000"):
+        monkeypatch.setenv("PI2_TC_BULK_MAX_TILES", tiles)
+        res[tiles] = P.RolloutEngine(model, cfg, device=0, noise="device").optimize_device(state, plan, cost, 1).controls
+    np.testing.assert_array_equal(res["0"], res["1000000"])
+
+
 def test_graph_replay_matches_eager_and_is_deterministic():
     params, model, cfg, task, state, plan, cost = _device_setup()
     g = P.RolloutEngine(model, cfg, device=0, noise="device", use_graph=True)
