@@ -180,6 +180,28 @@ int pi2_iterate_local(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t itera
                       double *rank_partial_dev, void *stream);
 int pi2_iterate_finalize(pi2_ctx *ctx, const double *gathered_partials_dev, int32_t world_size,
                          double temperature, void *stream);
+/* A rank's whole control step as one CUDA graph that the CALLER captures (the
+ * NCCL all-gather sits between the kernels), replacing the per-call staging and
+ * host synchronisation of pi2_iterate_local / pi2_load_plan / pi2_read_plan
+ * (controller.py:374-395 split at the update's reduction, controller.py:367-371):
+ *   pi2_stage_step            host only: state, keys, cost, plan -> pinned block
+ *                             (after the previous step's pi2_fetch_plan)
+ *   --- captured once, replayed every step on `stream` ---
+ *   pi2_enqueue_pull          pinned block -> device (args + plan)
+ *   per iteration:
+ *     pi2_iterate_local_staged   -> rank partial (device)
+ *     all-gather of the partials (caller, e.g. torch.distributed NCCL)
+ *     pi2_iterate_finalize       -> combine + plan update (device)
+ *   pi2_enqueue_push          device plan -> pinned block
+ *   ---
+ *   pi2_fetch_plan            synchronise `stream`, copy the plan out (host)
+ * The enqueue calls never synchronise or allocate, so they are capturable. */
+int pi2_stage_step(pi2_ctx *ctx, const double *state, const double *plan, const pi2_optimize_args *args);
+int pi2_enqueue_pull(pi2_ctx *ctx, void *stream);
+int pi2_iterate_local_staged(pi2_ctx *ctx, int32_t iteration, double temperature, double *rank_partial_dev,
+                             void *stream);
+int pi2_enqueue_push(pi2_ctx *ctx, void *stream);
+int pi2_fetch_plan(pi2_ctx *ctx, double *plan_out, void *stream);
 /* The same fixed-order partial combine on the host (no GPU needed):
  * partials (count, N, PI2_PARTIAL_WIDTH) -> out (N, PI2_PARTIAL_WIDTH). */
 int pi2_combine_partials_host(const double *partials, int64_t count, int32_t horizon_steps,

@@ -18,18 +18,14 @@ from .controller import (  # noqa: F401
     sample_dynamics_noise,
     sample_noise,
 )
-from .dynamics import (  # noqa: F401
-    AnalyticModel, Control, HybridModel, PerturbedModel, QuadParams, QuadState, Trajectory, propagate, step_analytic,
-    wrap_angle,
-)
+from .dynamics import AnalyticModel, Control, HybridModel, QuadParams, QuadState, wrap_angle  # noqa: F401
 from .lwpr import FrozenLwpr, LwprFormatError, LwprModel, ReceptiveField, load_model, save_model  # noqa: F401
-from .simworld import RolloutCost, Task, TrialResult, run_trial  # noqa: F401
+from .simworld import RolloutCost, Task  # noqa: F401
 
 __all__ = [
     "ControlPlan", "PiConfig", "RolloutBatch", "RolloutEngine", "evaluate_rollouts", "optimize",
     "path_integral_update", "receding_horizon_step", "sample_dynamics_noise", "sample_noise",
-    "AnalyticModel", "Control", "HybridModel", "PerturbedModel", "QuadParams", "QuadState", "Trajectory",
-    "propagate", "step_analytic", "wrap_angle",
+    "AnalyticModel", "Control", "HybridModel", "QuadParams", "QuadState", "wrap_angle",
     "FrozenLwpr", "LwprFormatError", "LwprModel", "ReceptiveField", "load_model", "save_model",
-    "RolloutCost", "Task", "TrialResult", "run_trial",
+    "RolloutCost", "Task",
 ]

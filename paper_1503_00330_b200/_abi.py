@@ -71,6 +71,11 @@ _SIGNATURES = {
     "pi2_read_plan": (C.c_int, [_P, _P, _P]),
     "pi2_iterate_local": (C.c_int, [_P, C.POINTER(OptimizeArgs), C.c_int32, _P, _P]),
     "pi2_iterate_finalize": (C.c_int, [_P, _P, C.c_int32, C.c_double, _P]),
+    "pi2_stage_step": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs)]),
+    "pi2_enqueue_pull": (C.c_int, [_P, _P]),
+    "pi2_iterate_local_staged": (C.c_int, [_P, C.c_int32, C.c_double, _P, _P]),
+    "pi2_enqueue_push": (C.c_int, [_P, _P]),
+    "pi2_fetch_plan": (C.c_int, [_P, _P, _P]),
     "pi2_combine_partials_host": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, _P]),
     "pi2_chunk_partials_host": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_double, _P]),
     "pi2_partial_chunk": (C.c_int64, []),

@@ -19,6 +19,7 @@ arrays), so results match the reference on identical inputs.
 from __future__ import annotations
 
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -334,7 +335,20 @@ def evaluate_rollouts(state, plan, noise, model, cost_model, sub_rollouts: int =
     return RolloutEngine(model, cfg, device=device).evaluate(state, plan, noise, cost_model, dyn_noise)
 
 
-_UPDATE_CTX: dict[int, _abi.Context] = {}
+# path_integral_update is a pure function in the reference; here it runs on a context
+# (stream + scratch), and contexts are one per host thread (include/pi2rh.h), so each
+# thread keeps its own per device.
+_UPDATE_TLS = threading.local()
+
+
+def _update_context(dev: int) -> _abi.Context:
+    ctxs = getattr(_UPDATE_TLS, "ctxs", None)
+    if ctxs is None:
+        ctxs = _UPDATE_TLS.ctxs = {}
+    ctx = ctxs.get(dev)
+    if ctx is None:
+        ctx = ctxs[dev] = _abi.Context(dev, 1, 1, 1)
+    return ctx
 
 
 def path_integral_update(plan: ControlPlan, batch: RolloutBatch, temperature: float,
@@ -347,9 +361,7 @@ def path_integral_update(plan: ControlPlan, batch: RolloutBatch, temperature: fl
     if not temperature > 0:
         raise ValueError("temperature must be positive")
     dev = _default_device() if device is None else int(device)
-    ctx = _UPDATE_CTX.get(dev)
-    if ctx is None:
-        ctx = _UPDATE_CTX[dev] = _abi.Context(dev, 1, 1, 1)
+    ctx = _update_context(dev)
     ctx.call("pi2_set_dynamics", dynamics_struct(QuadParams(), plan.lo, plan.hi))
     out = np.empty((len(plan), 4))
     ctx.call("pi2_update", int(costs.shape[0]), int(costs.shape[1]),

@@ -104,7 +104,7 @@ PI2_HD void partial_combine(double *a, const double *b, double neg_inv) {
 // wrap_angle: pi - mod(pi - a, 2 pi) with numpy float remainder semantics
 // (dynamics.py:27-29; npy_divmod: fmod, then a negative remainder shifted by +2 pi).  For |x| < 2 pi fmod(x, 2 pi) is x itself, so the common
 // path is branch-free (selects: no divergence between the lanes that run the three
-// angles); on [2 pi, 4 pi] it is the exact x - 2 pi (Sterbenz); anything else takes
+// angles); on [2 pi, 4 pi) it is the exact x - 2 pi (Sterbenz); anything else takes
 // the general, exact fmod.  Host and device compile the same IEEE operations
 // (tests/test_wrap_host.py checks the host build against numpy bit for bit).
 PI2_HD double wrap_angle(double a) {
@@ -114,7 +114,7 @@ PI2_HD double wrap_angle(double a) {
     // a zero remainder's sign (numpy makes it +0) cannot change pi - m
     m = x < 0.0 ? PI2_DADD(x, kTwoPi) : x;
   } else {
-    m = (x >= kTwoPi && x <= 2.0 * kTwoPi) ? PI2_DSUB(x, kTwoPi) : fmod(x, kTwoPi);
+    m = (x >= kTwoPi && x < 2.0 * kTwoPi) ? PI2_DSUB(x, kTwoPi) : fmod(x, kTwoPi);  // 4 pi itself: fmod -> 0
     if (m != 0.0) {
       if (m < 0.0) m = PI2_DADD(m, kTwoPi);
     } else {

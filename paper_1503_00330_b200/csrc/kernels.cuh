@@ -568,7 +568,8 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
 #endif
 constexpr int kRoll1Unroll = PI2_ROLL1_UNROLL;
 
-// MM: compile-time sub-rollouts held in registers (1), or 0 = runtime M <= PI2_MAX_SUB_ROLLOUTS.
+// MM: compile-time sub-rollouts held in registers (1; more than one sub-rollout per
+// rollout runs rollout_group_kernel, up to PI2_MAX_SUB_ROLLOUTS on 32 lanes).
 // FAST: hybrid LWPR model + navigation cost, branches folded at compile time.
 template <int MM, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
@@ -611,8 +612,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
   if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, k);
   if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, k);
-  float4 apn = (1 < N) ? __ldg(a.xin + a.K + k) : __ldg(a.ang_last + k);
-  float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 apn = (1 < N) ? __ldcg(a.xin + a.K + k) : __ldcg(a.ang_last + k);
+  float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldcg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll(kRoll1Unroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
     if (t + 1 < N) {
       if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
       if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
-      apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + k);
+      apn = (t + 2 < N) ? __ldcg(a.xin + row + 2 * a.K) : __ldcg(a.ang_last + k);
     }
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
     if (hybrid) {
@@ -737,29 +738,36 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
 constexpr int kRollUnroll = PI2_ROLL_UNROLL;
 
 // Sub-rollouts on lanes: a group of G lanes (G = S rounded up to a power of
-// two, <= 32) per rollout, lane m integrating sub-rollout m.  The M-mean is
+// two, <= 32) per rollout, lane m integrating sub-rollout m; G = 64 (33 <= S
+// <= 64) runs 32 lanes holding sub-rollouts m and m + 32 each.  The M-mean is
 // the reference's pairwise tree (controller.py:314-319): for S == G an xor
 // butterfly reproduces it exactly (adjacent pairs at every level, IEEE add
-// is commutative); otherwise lane 0 replays the reference loop from shared
-// memory.  Lane 0 of the group owns the float64 suffix sum.
+// is commutative; with two slots per lane the butterfly leaves the means of
+// 0..31 and 32..63, the tree's last pair); otherwise lane 0 replays the
+// reference loop from shared memory.  Lane 0 of the group owns the float64
+// suffix sum.
 // FAST: hybrid LWPR model, device dynamics noise, navigation cost (the
 // real-time configuration) with every branch folded at compile time.
 template <int G, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a) {
-  constexpr int RPB = kRolloutBlock / G;  // rollouts per block
+  constexpr int SPL = G > 32 ? 2 : 1;     // sub-rollouts per lane
+  constexpr int GL = G / SPL;             // lanes per rollout
+  constexpr int RPB = kRolloutBlock / GL;  // rollouts per block
   extern __shared__ float sq[];           // (N, RPB) stage costs
-  __shared__ float qbuf[kRolloutBlock];
+  __shared__ float qbuf[kRolloutBlock * SPL];
   __shared__ pi2_cost cost;
   if (threadIdx.x == 0) cost = a.sa->cost;
   __syncthreads();
   pdl_wait();
-  const int lane_g = threadIdx.x % G, grp = threadIdx.x / G;
+  const int lane_g = threadIdx.x % GL, grp = threadIdx.x / GL;
   const int64_t k = (int64_t)blockIdx.x * RPB + grp;
   const bool live = k < a.K;
   const int S = a.M;
   const int N = a.N;
-  const bool active = live && lane_g < S;
-  const int m = lane_g;
+  bool act[SPL];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) act[j] = live && lane_g + j * GL < S;
+  const bool active = act[0];
   const StepArgs *sa = a.sa;
   const float p0[3] = {__double2float_rn(sa->state[0]), __double2float_rn(sa->state[1]),
                        __double2float_rn(sa->state[2])};
@@ -773,10 +781,17 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   const int64_t kk = live ? k : 0;
   const bool device_dyn = FAST || a.device_dyn;
   const bool two_point = !FAST && a.model == PI2_MODEL_TWO_POINT;
-  const uint64_t dyn_base = (kg * (uint64_t)S + (uint64_t)m) * (uint64_t)N;  // counter of (k, m, t=0)
+  // counter of (k, m, t=0) of each slot's sub-rollout m = lane_g + j * GL
+  const uint64_t dyn_base = (kg * (uint64_t)S + (uint64_t)lane_g) * (uint64_t)N;
 
-  float cs[3] = {-0.0f, -0.0f, -0.0f}, ccs[3] = {-0.0f, -0.0f, -0.0f};
-  bool crashed = false;
+  float cs[SPL][3], ccs[SPL][3];
+  bool crashed[SPL];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) {
+    crashed[j] = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cs[j][c] = ccs[j][c] = -0.0f;  // -0 + x == x: cumsum start
+  }
   const bool hybrid = FAST || a.model == PI2_MODEL_HYBRID_LWPR;
   // rows of step t+1 are loaded while step t computes (hides HBM latency)
   float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
@@ -786,7 +801,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       m4n = ld_planes(a.lw_mean, a.lw_plane, kk);
       s4n = ld_planes(a.lw_std, a.lw_plane, kk);
     }
-    apn = (1 < N) ? __ldg(a.xin + a.K + kk) : __ldg(a.ang_last + kk);
+    apn = (1 < N) ? __ldcg(a.xin + a.K + kk) : __ldcg(a.ang_last + kk);
   }
 #pragma unroll(kRollUnroll)
   for (int t = 0; t < N; ++t) {
@@ -798,9 +813,11 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
         m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
         s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
       }
-      apn = (t + 2 < N) ? __ldg(a.xin + row + 2 * a.K) : __ldg(a.ang_last + kk);
+      apn = (t + 2 < N) ? __ldcg(a.xin + row + 2 * a.K) : __ldcg(a.ang_last + kk);
     }
-    float q = 0.0f;
+    float q[SPL];
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) q[j] = 0.0f;
     if (active) {
       float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
       if (hybrid) {
@@ -817,47 +834,57 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       // a write-after-write stall of a full DRAM latency per step (ncu, rollout kernel)
       angterm = fmaf(ap.w, 0.0f, angterm);
       const float sdt = __fmul_rn(a.dp.dt32, (float)(t + 1));
-      float d[3];
-      if (device_dyn) {
-        const float4 z = normals4(dyn_base + (uint64_t)t, dk0, dk1);
-        d[0] = z.x; d[1] = z.y; d[2] = z.z;
-      } else {
-        const float *dp = a.dyn + ((kk * S + m) * (int64_t)N + t) * 3;
-        d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
-      }
-      if (two_point) {
-        d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
-      }
-      float pos[3], vel[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float acc = __fadd_rn(__fmul_rn(sd[c], d[c]), mn[c]);
-        cs[c] = __fadd_rn(cs[c], acc);
-        ccs[c] = __fadd_rn(ccs[c], cs[c]);
-        vel[c] = __fadd_rn(__fmul_rn(cs[c], a.dp.dt32), v0[c]);
-        pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[c], cs[c]), a.dp.dt2_32), __fmul_rn(sdt, v0[c])),
-                           p0[c]);
-      }
-      if (threshold_cost) {
-        q = pos[2] > cost.threshold ? 1.0f : 0.0f;
-      } else {
-        crashed = crashed | nav_crash_now(nav, pos[0], pos[1], pos[2]);  // no short-circuit branch
-        q = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed);
+      for (int j = 0; j < SPL; ++j) {
+        if (!act[j]) continue;
+        const int m = lane_g + j * GL;
+        float d[3];
+        if (device_dyn) {
+          const float4 z = normals4(dyn_base + (uint64_t)(j * GL) * (uint64_t)N + (uint64_t)t, dk0, dk1);
+          d[0] = z.x; d[1] = z.y; d[2] = z.z;
+        } else {
+          const float *dp = a.dyn + ((kk * S + m) * (int64_t)N + t) * 3;
+          d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
+        }
+        if (two_point) {
+          d[0] = sign_of(d[0]); d[1] = sign_of(d[1]); d[2] = sign_of(d[2]);
+        }
+        float pos[3], vel[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float acc = __fadd_rn(__fmul_rn(sd[c], d[c]), mn[c]);
+          cs[j][c] = __fadd_rn(cs[j][c], acc);
+          ccs[j][c] = __fadd_rn(ccs[j][c], cs[j][c]);
+          vel[c] = __fadd_rn(__fmul_rn(cs[j][c], a.dp.dt32), v0[c]);
+          pos[c] = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(ccs[j][c], cs[j][c]), a.dp.dt2_32),
+                                       __fmul_rn(sdt, v0[c])),
+                             p0[c]);
+        }
+        if (threshold_cost) {
+          q[j] = pos[2] > cost.threshold ? 1.0f : 0.0f;
+        } else {
+          crashed[j] = crashed[j] | nav_crash_now(nav, pos[0], pos[1], pos[2]);  // no short-circuit branch
+          q[j] = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[j]);
+        }
       }
     }
     float qm;
     if (S == G) {
 #pragma unroll
-      for (int off = 1; off < G; off <<= 1) q = __fmul_rn(0.5f, __fadd_rn(q, __shfl_xor_sync(0xffffffffu, q, off)));
-      qm = q;
+      for (int j = 0; j < SPL; ++j)
+#pragma unroll
+        for (int off = 1; off < GL; off <<= 1)
+          q[j] = __fmul_rn(0.5f, __fadd_rn(q[j], __shfl_xor_sync(0xffffffffu, q[j], off)));
+      qm = SPL == 1 ? q[0] : __fmul_rn(0.5f, __fadd_rn(q[0], q[SPL - 1]));
     } else {
-      qbuf[threadIdx.x] = q;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) qbuf[j * kRolloutBlock + threadIdx.x] = q[j];
       __syncwarp();
       qm = 0.0f;
       if (lane_g == 0) {
         float v[G];
 #pragma unroll
-        for (int i = 0; i < G; ++i) v[i] = qbuf[threadIdx.x + i];
+        for (int i = 0; i < G; ++i) v[i] = qbuf[(i / GL) * kRolloutBlock + threadIdx.x + i % GL];
         int n = S;
         while (n > 1) {
           if ((n & 1) == 0) {
@@ -881,8 +908,11 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
     if (lane_g == 0) sq[t * RPB + grp] = qm;
   }
   // persistent crash of any sub-rollout (controller.py:310)
-  const unsigned ballot = __ballot_sync(0xffffffffu, crashed);
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x % 32) / G * G));
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) any = any || crashed[j];
+  const unsigned ballot = __ballot_sync(0xffffffffu, any);
+  const unsigned gmask = (GL == 32) ? 0xffffffffu : (((1u << GL) - 1u) << ((threadIdx.x % 32) / GL * GL));
   bool crash = (ballot & gmask) != 0;
   if (!live || lane_g != 0) return;
   const double dt = a.dp.dt, ceiling = sa->ceiling;
@@ -987,7 +1017,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
       const float3 m4 = ld_planes(a.lw_mean, a.lw_plane, row);
       mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
     } else if (model == PI2_MODEL_ANALYTIC) {
-      const float4 xr = __ldg(a.xin + row);
+      const float4 xr = __ldcg(a.xin + row);
       float sr, cr, sp, cp, sy, cy;
       sincosf(xr.x, &sr, &cr);
       sincosf(xr.y, &sp, &cp);
@@ -1001,7 +1031,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
       mn[0] = mn[1] = mn[2] = 0.0f;
     }
     acc[3 * t] = mn[0]; acc[3 * t + 1] = mn[1]; acc[3 * t + 2] = mn[2];
-    const float4 ap = (t + 1 < N) ? __ldg(a.xin + row + a.K) : __ldg(a.ang_last + k);
+    const float4 ap = (t + 1 < N) ? __ldcg(a.xin + row + a.K) : __ldcg(a.ang_last + k);
     angt[t] = __fmul_rn(__fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)),
                         0.2f);
   }

@@ -347,7 +347,7 @@ int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
 template <int G, bool FAST>
 int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   auto *fn = rollout_group_kernel<G, FAST>;
-  constexpr int RPB = kRolloutBlock / G;
+  constexpr int RPB = kRolloutBlock / (G > 32 ? 32 : G);
   const int smem = a.N * RPB * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + RPB - 1) / RPB;
@@ -365,14 +365,16 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int S = a.spread ? a.M : 1;
   const bool nav = ctx->cost.kind == PI2_COST_NAVIGATION;
   const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
-  // sub-rollouts on lanes (any model but the analytic one, which is never spread)
-  if (S > 1 && S <= 32) {
+  // sub-rollouts on lanes (any model but the analytic one, which is never spread);
+  // 33..64 on 32 lanes with two each (S <= PI2_MAX_SUB_ROLLOUTS = 64)
+  if (S > 1) {
     const bool fast = hybrid && nav && a.device_dyn;
     if (S <= 2) return launch_group_g<2>(ctx, a, fast, st);
     if (S <= 4) return launch_group_g<4>(ctx, a, fast, st);
     if (S <= 8) return launch_group_g<8>(ctx, a, fast, st);
     if (S <= 16) return launch_group_g<16>(ctx, a, fast, st);
-    return launch_group_g<32>(ctx, a, fast, st);
+    if (S <= 32) return launch_group_g<32>(ctx, a, fast, st);
+    return launch_group_g<64>(ctx, a, fast, st);
   }
   if (S == 1 && a.K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
     const unsigned grid = (unsigned)((a.K + kWideWarps - 1) / kWideWarps);
@@ -387,8 +389,7 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     CU(cudaGetLastError());
     return PI2_OK;
   }
-  if (S == 1) return (hybrid && nav) ? launch_rollout_t<1, true>(ctx, a, st) : launch_rollout_t<1, false>(ctx, a, st);
-  return launch_rollout_t<0, false>(ctx, a, st);
+  return (hybrid && nav) ? launch_rollout_t<1, true>(ctx, a, st) : launch_rollout_t<1, false>(ctx, a, st);
 }
 
 int check_ready(pi2_ctx *ctx) {
@@ -982,6 +983,62 @@ int pi2_iterate_local(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t itera
   TRY(ensure_params(ctx));
   TRY(stage_args(ctx, nullptr, args, args->cost_ceiling, st));
   return launch_iteration(ctx, iteration, -1.0 / args->temperature, root_dev, false, st);
+}
+
+// ---- a rank's control step as one caller-captured CUDA graph (N > 1) ----------
+// The collective sits between the kernels, so the caller (torch.distributed) owns
+// the graph; these calls only enqueue work on `stream` (no host synchronisation,
+// no allocation), so they can be captured together with the NCCL all-gather.
+int pi2_stage_step(pi2_ctx *ctx, const double *state, const double *plan, const pi2_optimize_args *args) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (!state || !plan) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(ensure_params(ctx));  // model staging happens here, never inside a capture
+  CU(cudaEventSynchronize(ctx->staged));
+  fill_args(ctx, state, args, args->cost_ceiling);
+  std::memcpy(ctx->h_plan, plan, sizeof(double) * 4 * ctx->N);
+  return PI2_OK;
+}
+
+int pi2_enqueue_pull(pi2_ctx *ctx, void *stream) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  TRY(bind(ctx));
+  cudaStream_t st = pick(ctx, stream);
+  const size_t bytes = kIoArgsBytes + sizeof(double) * 4 * ctx->N;
+  if (ctx->uva && ctx->io_pull) {
+    io_pull_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint4 *>(ctx->h_io), reinterpret_cast<uint4 *>(ctx->d_io),
+                                      (int)(bytes / sizeof(uint4)));
+    CU(cudaGetLastError());
+  } else {
+    CU(cudaMemcpyAsync(ctx->d_io, ctx->h_io, bytes, cudaMemcpyHostToDevice, st));
+  }
+  return PI2_OK;
+}
+
+int pi2_iterate_local_staged(pi2_ctx *ctx, int32_t iteration, double temperature, double *root_dev, void *stream) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  if (iteration < 0 || !root_dev) return fail(ctx, PI2_ERR_INVALID, "bad iteration index or null partial buffer");
+  if (!(temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
+  if (ctx->params_dirty) return fail(ctx, PI2_ERR_STATE, "model changed since pi2_stage_step");
+  return launch_iteration(ctx, iteration, -1.0 / temperature, root_dev, false, pick(ctx, stream));
+}
+
+int pi2_enqueue_push(pi2_ctx *ctx, void *stream) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  TRY(bind(ctx));
+  CU(cudaMemcpyAsync(ctx->h_plan, ctx->d_plan, sizeof(double) * 4 * ctx->N, cudaMemcpyDeviceToHost,
+                     pick(ctx, stream)));
+  return PI2_OK;
+}
+
+int pi2_fetch_plan(pi2_ctx *ctx, double *plan_out, void *stream) {
+  if (!ctx || !plan_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(bind(ctx));
+  CU(cudaStreamSynchronize(pick(ctx, stream)));
+  std::memcpy(plan_out, ctx->h_plan, sizeof(double) * 4 * ctx->N);
+  return PI2_OK;
 }
 
 int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double *mufu_share) {

@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _abi
-from .controller import ControlPlan, PiConfig, dynamics_struct, model_kind, optimize_args
+from .controller import ControlPlan, PiConfig, _cost_key, dynamics_struct, model_kind, optimize_args
 from .lwpr import stage_axis
 from .simworld import cost_struct
 
@@ -73,9 +73,18 @@ class ShardedEngine:
     ``optimize(state, plan, cost_model, cycle_index)`` has the semantics of
     ``controller.optimize`` with a ``noise="device"`` engine; all ranks return
     the same plan.
+
+    With NCCL (``use_graph`` default) the rank's whole control step — input pull,
+    per iteration local kernels -> ``all_gather_into_tensor`` -> combine + plan
+    update, plan push — is captured once into one CUDA graph (torch.cuda.graph,
+    NCCL collectives are capturable) and replayed every step: one graph launch
+    and one stream synchronisation per control step, no per-iteration host
+    round trip.  The gloo backend (CPU tests, several ranks sharing one GPU)
+    runs the same calls eagerly with the exchange staged through the host.
     """
 
-    def __init__(self, model, config: PiConfig, group=None, device: int | None = None):
+    def __init__(self, model, config: PiConfig, group=None, device: int | None = None,
+                 use_graph: bool | None = None):
         import torch
         import torch.distributed as dist
 
@@ -98,22 +107,77 @@ class ShardedEngine:
                 stage_axis(self.ctx, a, model.models[a])
         self.ctx.call("pi2_select_model", kind, param)
         dev = torch.device("cuda", self.device)
-        self.partial = torch.empty((config.horizon_steps, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=dev)
+        n = config.horizon_steps
+        self.partial = torch.empty((n, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=dev)
+        self.gathered = torch.empty((self.world, n, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=dev)
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.use_graph = self.nccl if use_graph is None else bool(use_graph and self.nccl)
+        self._graph = None
+        self._graph_key = None
+        self._bound = None
+        self._plan_buf = np.empty((n, 4))
+        self._state_buf = np.empty(12)
+        self.graph_captures = 0
+
+    def _bind(self, plan, cost_model) -> None:
+        key = (np.asarray(plan.lo, float).tobytes(), np.asarray(plan.hi, float).tobytes(), _cost_key(cost_model))
+        if key == self._bound and key[-1] is not None:
+            return
+        self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
+        self.ctx.call("pi2_set_cost", cost_struct(cost_model))
+        self._bound = key
+
+    def _enqueue_step(self, iterations: int, temperature: float, stream) -> None:
+        """The step's device work on ``stream``: pull, iterations with the exchange, push."""
+        import torch.distributed as dist
+
+        self.ctx.call("pi2_enqueue_pull", stream)
+        for it in range(iterations):
+            self.ctx.call("pi2_iterate_local_staged", it, temperature, _abi.ptr(self.partial), stream)
+            dist.all_gather_into_tensor(self.gathered, self.partial, group=self.group)
+            self.ctx.call("pi2_iterate_finalize", _abi.ptr(self.gathered), self.world, temperature, stream)
+        self.ctx.call("pi2_enqueue_push", stream)
+
+    def _capture(self, iterations: int, temperature: float):
+        import torch
+        import torch.distributed as dist
+
+        # the communicator must exist before capture: one eager collective
+        dist.all_gather_into_tensor(self.gathered, self.partial, group=self.group)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+            self._enqueue_step(iterations, temperature, _abi.torch_stream(self.device))
+        self.graph_captures += 1
+        return g
 
     def optimize(self, state, plan: ControlPlan, cost_model, cycle_index: int = 0) -> ControlPlan:
         cfg = self.config
         if cfg.iterations_per_step == 0:
             return plan
+        self._bind(plan, cost_model)
+        args = optimize_args(cfg, cycle_index, use_graph=self.use_graph)
+        st = self._state_buf
+        st[0:3], st[3:6], st[6:9], st[9:12] = state.position, state.velocity, state.angles, state.rates
+        self._plan_buf[...] = plan.controls
+        self.ctx.call("pi2_stage_step", _abi.ptr(st), _abi.ptr(self._plan_buf), args)
         stream = _abi.torch_stream(self.device)
-        self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
-        self.ctx.call("pi2_set_cost", cost_struct(cost_model))
-        args = optimize_args(cfg, cycle_index, use_graph=False)
-        controls = np.ascontiguousarray(plan.controls, dtype=np.float64).copy()
-        self.ctx.call("pi2_load_plan", _abi.ptr(np.ascontiguousarray(state.as_array())), _abi.ptr(controls),
-                      stream)
-        for it in range(cfg.iterations_per_step):
-            self.ctx.call("pi2_iterate_local", args, it, _abi.ptr(self.partial), stream)
-            gathered = gather_partials(self.partial, self.group)
-            self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, float(cfg.temperature), stream)
-        self.ctx.call("pi2_read_plan", _abi.ptr(controls), stream)
-        return plan.replaced(controls)
+        temperature = float(cfg.temperature)
+        if self.use_graph:
+            key = (int(cfg.iterations_per_step), temperature)
+            if self._graph is None or self._graph_key != key:
+                self._graph, self._graph_key = self._capture(*key), key
+            self._graph.replay()
+        elif self.nccl:
+            self._enqueue_step(int(cfg.iterations_per_step), temperature, stream)
+        else:  # gloo: the exchange goes through the host
+            self.ctx.call("pi2_enqueue_pull", stream)
+            for it in range(cfg.iterations_per_step):
+                self.ctx.call("pi2_iterate_local_staged", it, temperature, _abi.ptr(self.partial), stream)
+                gathered = gather_partials(self.partial, self.group)
+                self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, temperature, stream)
+            self.ctx.call("pi2_enqueue_push", stream)
+        out = np.empty_like(self._plan_buf)
+        self.ctx.call("pi2_fetch_plan", _abi.ptr(out), stream)
+        return plan.replaced(out)

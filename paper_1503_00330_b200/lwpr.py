@@ -41,16 +41,50 @@ class ReceptiveField:
     inv_gram: np.ndarray = field(default=None)
 
 
-class LwprModel:
-    """Receptive-field container with the reference's stacking accessor."""
+def _metric_of(d_init, dim: int) -> np.ndarray:
+    """d_init as a (dim, dim) metric: scalar -> scaled identity, vector -> diagonal,
+    matrix -> its symmetric part (the reference's normalisation, lwpr.py:35-50)."""
+    d = np.asarray(d_init, float)
+    if d.ndim == 0:
+        return float(d) * np.eye(dim)
+    if d.shape == (dim,):
+        return np.diag(d)
+    if d.shape == (dim, dim):
+        return 0.5 * (d + d.T)
+    if d.ndim == 1:
+        raise ValueError(f"d_init vector must have length {dim}")
+    raise ValueError(f"d_init must be scalar, ({dim},) or ({dim},{dim})")
 
-    def __init__(self, input_dim: int, hyperparams: dict | None = None):
+
+class LwprModel:
+    """Receptive-field container with the reference's constructor (lwpr.py:100-124:
+    same keywords, defaults and validation) and stacking accessor.  The
+    hyperparameters only matter to training, which stays on the host in the
+    reference; here they are carried for persistence (``save_model``)."""
+
+    def __init__(self, input_dim: int, w_gen: float = 0.1, d_init=1.0, forgetting: float = 1.0,
+                 ridge: float = 1e-3, participation: float = 1e-3):
         if input_dim < 1:
             raise ValueError("input_dim must be >= 1")
+        if not 0.0 < w_gen < 1.0:
+            raise ValueError("w_gen must be in (0, 1)")
+        if not 0.0 < forgetting <= 1.0:
+            raise ValueError("forgetting must be in (0, 1]")
+        if ridge < 0.0:
+            raise ValueError("ridge must be >= 0")
         self.input_dim = int(input_dim)
-        self.hyperparams = dict(hyperparams or {})
+        self.w_gen = float(w_gen)
+        self.d_init = _metric_of(d_init, self.input_dim)
+        self.forgetting = float(forgetting)
+        self.ridge = float(ridge)
+        self.participation = float(participation)
         self.fields: list[ReceptiveField] = []
         self._stacked = None
+
+    @property
+    def hyperparams(self) -> dict:
+        return {"w_gen": self.w_gen, "d_init": self.d_init, "forgetting": self.forgetting, "ridge": self.ridge,
+                "participation": self.participation}
 
     @classmethod
     def from_stack(cls, centers, metrics, coefs, lvar) -> "LwprModel":
@@ -89,8 +123,9 @@ def stacks_of(model):
 
 def save_model(model: LwprModel) -> bytes:
     """Serialise in the reference's "LWPR1" format (lwpr.py:261-285)."""
-    hp = model.hyperparams or {}
     d = model.input_dim
+    hp = {k: getattr(model, k) for k in ("w_gen", "d_init", "forgetting", "ridge", "participation")
+          if hasattr(model, k)}
     payload = {
         "input_dim": d,
         "hyperparams": {
@@ -127,7 +162,10 @@ def load_model(data: bytes) -> LwprModel:
     except (json.JSONDecodeError, UnicodeDecodeError) as e:
         raise LwprFormatError(f"invalid payload: {e}", offset=off + getattr(e, "pos", 0)) from e
     try:
-        model = LwprModel(int(payload["input_dim"]), dict(payload["hyperparams"]))
+        hp = payload["hyperparams"]
+        model = LwprModel(int(payload["input_dim"]), w_gen=float(hp["w_gen"]),
+                          d_init=np.array(hp["d_init"], dtype=np.float64), forgetting=float(hp["forgetting"]),
+                          ridge=float(hp["ridge"]), participation=float(hp["participation"]))
         for fd in payload["fields"]:
             model.fields.append(ReceptiveField(
                 center=np.array(fd["center"], dtype=np.float64),

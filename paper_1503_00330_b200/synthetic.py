@@ -132,3 +132,46 @@ CONFIGS = {
     "C4": dict(K=1 << 20, T=50, L=100, M=1),
     "C5": dict(K=1 << 22, T=50, L=200, M=1),
 }
+
+
+# ---------------------------------------------------------------- the reference's objects
+def import_reference():
+    """The reference package ``pimpc`` (for the drop-in tests, the closed-loop bench and
+    the reference arm): already importable, else the copy installed under
+    ``baseline/_ref`` (pip --target from /root/reference; it travels to the GPU box),
+    else the source tree.  Returns a namespace with ``controller``, ``dynamics``,
+    ``lwpr``, ``simworld``, or None when the reference is not present."""
+    import importlib
+    import os
+    import sys
+    import types
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for path in (None, os.path.join(root, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if path is not None:
+            if not os.path.isdir(os.path.join(path, "pimpc")):
+                continue
+            if path not in sys.path:
+                sys.path.append(path)
+        try:
+            mods = {n: importlib.import_module(f"pimpc.{n}") for n in ("controller", "dynamics", "lwpr", "simworld")}
+        except ImportError:
+            continue
+        return types.SimpleNamespace(**mods)
+    return None
+
+
+def reference_hybrid(ref, stacks, params=None):
+    """A reference ``HybridModel`` (dynamics.py:214-235) holding exactly these receptive
+    fields (built field by field, as the reference's own tests build models,
+    tests/oracles.py:47-67)."""
+    models = []
+    for s in stacks:
+        m = ref.lwpr.LwprModel(input_dim=s.centers.shape[1])
+        for i in range(s.num_fields):
+            m.fields.append(ref.lwpr.ReceptiveField(
+                center=s.centers[i].copy(), metric=s.metrics[i].copy(), coef=s.coefs[i].copy(),
+                local_variance=float(s.lvar[i]), inv_gram=np.eye(s.centers.shape[1] + 1)))
+        m._stacked = None
+        models.append(m)
+    return ref.dynamics.HybridModel(tuple(models), params or ref.dynamics.QuadParams())

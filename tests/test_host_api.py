@@ -8,7 +8,7 @@ import paper_1503_00330_b200 as P
 from paper_1503_00330_b200 import _abi
 from paper_1503_00330_b200.controller import model_kind
 from paper_1503_00330_b200.lwpr import LwprFormatError, stacks_of
-from paper_1503_00330_b200.simworld import cost_struct, closest_pass_metric
+from paper_1503_00330_b200.simworld import cost_struct
 from tests._cases import load
 
 
@@ -58,8 +58,10 @@ def test_plugin_classification():
     assert model_kind(P.AnalyticModel(p))[0] == _abi.MODEL_ANALYTIC
     assert model_kind(P.HybridModel.from_stacks(
         __import__("paper_1503_00330_b200.synthetic", fromlist=["x"]).hybrid_stacks(4), p))[0] == _abi.MODEL_HYBRID_LWPR
+    class Perturbed:  # the reference's ground-truth PerturbedModel (dynamics.py:190-211)
+        params, probabilistic, drag_coeff = p, False, 0.1
     with pytest.raises(TypeError, match="velocity-dependent"):
-        model_kind(P.PerturbedModel(p, drag_coeff=0.1))
+        model_kind(Perturbed())
 
     class Weird:
         params = p
@@ -72,60 +74,42 @@ def test_plugin_classification():
         cost_struct(object())
 
 
-def test_closest_pass_metric_matches_definition():
-    xs = np.linspace(-1.5, 1.5, 200)
-    pos = np.stack([xs, np.full_like(xs, -0.9), np.ones_like(xs)], 1)
-    passes, avg = closest_pass_metric(pos, np.array([[0.0, -0.9]]))
-    assert len(passes) == 1 and passes[0] == pytest.approx(np.abs(xs).min())
-    assert avg == passes[0]
+def test_lwpr_model_reference_constructor():
+    """LwprModel takes the reference's keyword constructor (lwpr.py:100-124): same
+    defaults, validation and d_init normalisation, and round-trips through LWPR1."""
+    m = P.LwprModel(input_dim=4, d_init=[30.0, 30.0, 30.0, 1500.0], ridge=1e-4)
+    np.testing.assert_array_equal(m.d_init, np.diag([30.0, 30.0, 30.0, 1500.0]))
+    assert (m.w_gen, m.forgetting, m.ridge, m.participation) == (0.1, 1.0, 1e-4, 1e-3)
+    np.testing.assert_array_equal(P.LwprModel(2, d_init=3.0).d_init, 3.0 * np.eye(2))
+    np.testing.assert_array_equal(P.LwprModel(2, d_init=[[1.0, 2.0], [0.0, 1.0]]).d_init, [[1.0, 1.0], [1.0, 1.0]])
+    for kw, msg in [(dict(input_dim=0), "input_dim"), (dict(input_dim=2, w_gen=1.0), "w_gen"),
+                    (dict(input_dim=2, forgetting=0.0), "forgetting"), (dict(input_dim=2, ridge=-1.0), "ridge"),
+                    (dict(input_dim=2, d_init=[1.0, 2.0, 3.0]), "length 2"),
+                    (dict(input_dim=2, d_init=np.ones((2, 3))), "d_init must be")]:
+        with pytest.raises(ValueError, match=msg):
+            P.LwprModel(**kw)
+    m.fields.append(P.ReceptiveField(np.zeros(4), np.diag([30.0, 30.0, 30.0, 1500.0]), np.arange(5.0), 0.02,
+                                     inv_gram=np.eye(5)))
+    m2 = P.load_model(P.save_model(m))
+    assert (m2.w_gen, m2.ridge) == (0.1, 1e-4)
+    np.testing.assert_array_equal(m2.d_init, m.d_init)
+    for a, b in zip(stacks_of(m2), stacks_of(m)):
+        np.testing.assert_array_equal(a, b)
 
 
-def test_plant_step_matches_reference_euler():
-    p = P.QuadParams()
-    st = P.QuadState(np.array([0.1, 0.2, 1.0]), np.array([0.3, -0.1, 0.0]), np.array([0.05, -0.02, 0.1]),
-                     np.array([0.5, 0.0, -0.2]))
-    c = p.control([1.0, -2.0, 0.5], 0.2)
-    nxt = P.AnalyticModel(p).step(st, c)
-    np.testing.assert_array_equal(nxt.position, st.position + st.velocity * p.dt)
-    np.testing.assert_allclose(nxt.rates, st.rates + p.rate_gain * (c.desired_rates - st.rates) * p.dt)
+def test_dropin_patch_restores_reference_module():
+    """dropin.patched swaps the engine and step of a controller module for the block only."""
+    import types
 
+    from paper_1503_00330_b200 import dropin
 
-def _propagate_inputs(z):
-    p = P.QuadParams()
-    plan = P.ControlPlan(z["plan"], p.dt, 0.0, *p.control_bounds())
-    return p, plan, P.QuadState.from_array(z["state"])
-
-
-@pytest.mark.parametrize("name", ["analytic", "perturbed"])
-def test_propagate_matches_reference(name):
-    """dynamics.propagate (dynamics.py:305-342) with the host models: bitwise."""
-    z = load("propagate")
-    p, plan, state = _propagate_inputs(z)
-    model = P.AnalyticModel(p) if name == "analytic" else P.PerturbedModel(p, drag_coeff=0.08, thrust_scale=0.97)
-    tr = P.propagate(model, state, plan, 30)
-    np.testing.assert_array_equal(tr.states, z[name + "_states"])
-    assert tr.diverged == bool(z[name + "_diverged"])
-    np.testing.assert_array_equal(tr.positions, tr.states[:, :3])
-    np.testing.assert_array_equal(tr.final_state().as_array(), tr.states[-1])
-    # the same through step_analytic for the analytic model
-    if name == "analytic":
-        s = state
-        for i in range(30):
-            s = P.step_analytic(s, p.control(plan.controls[i, :3], plan.controls[i, 3]), p)
-        np.testing.assert_array_equal(s.as_array(), tr.states[-1])
-
-
-def test_propagate_divergence_and_errors():
-    z = load("propagate")
-    p, plan, state = _propagate_inputs(z)
-    wild = np.tile([0.0, 0.0, 0.0, p.f_max], (30, 1))
-    tr = P.propagate(P.AnalyticModel(p), state, wild, 30, sanity_box=np.array([1.0, 1.0, 1.5]))
-    np.testing.assert_array_equal(tr.states, z["wild_states"])
-    assert tr.diverged and bool(z["wild_diverged"])
-    with pytest.raises(ValueError, match="exceeds plan length"):
-        P.propagate(P.AnalyticModel(p), state, plan, 31)
-    with pytest.raises(ValueError, match="requires noise"):
-        P.propagate(P.AnalyticModel(p), state, plan, 30, mode="sample")
-    with pytest.raises(TypeError, match="velocity-dependent"):
-        P.PerturbedModel(p, drag_coeff=0.1).make_batch_eval(8)
+    mod = types.SimpleNamespace(RolloutEngine="ref-engine", receding_horizon_step="ref-step")
+    times = []
+    with dropin.patched(mod, noise="device", device=0, step_times=times):
+        assert mod.RolloutEngine.func is P.RolloutEngine
+        assert mod.RolloutEngine.keywords == {"noise": "device", "device": 0, "use_graph": True}
+        assert mod.receding_horizon_step is not P.receding_horizon_step  # timed wrapper
+    assert (mod.RolloutEngine, mod.receding_horizon_step) == ("ref-engine", "ref-step")
+    with dropin.patched(mod, noise="reference", replace_step=False):
+        assert mod.receding_horizon_step == "ref-step"
     assert P.Task.default().total_switches == 3 * 4

@@ -1,8 +1,9 @@
-"""Design check behind DESIGN.md "Why not the tensor cores (yet)": a numpy
-emulation of the FlashAttention-shaped tensor-core LWPR (3xTF32 logit GEMM ->
-exp -> 3xTF32 moment GEMM P.V) stays within 1e-5 absolute of the reference's
-float32 fast path on realistic rollout rows, i.e. the numerics would pass the
-cost gate; the decision against it is throughput, not precision."""
+"""Numerics of the tensor-core LWPR (csrc/lwpr_tc.cuh, the default LWPR kernel for
+shared-metric models), emulated in numpy: the 3xTF32 logit GEMM -> exp -> a 3xTF32
+moment GEMM P.V (the FlashAttention-shaped form; the kernel keeps the moments on
+the CUDA cores, the emulation also covers moving them onto the tensor cores) stays
+within 1e-5 absolute of the reference's float32 fast path on realistic rollout rows,
+i.e. within the cost gate.  The GPU parity suite checks the kernel itself."""
 
 import numpy as np
 

@@ -43,7 +43,8 @@ def test_wrap_angle_host_build_matches_numpy(wrap_bin, tmp_path):
     edge = [0.0, -0.0, pi, -pi, tau, -tau, 2 * tau, -2 * tau, 3 * tau, pi + tau, pi - tau, pi + 2 * tau,
             np.nextafter(pi, 0), np.nextafter(pi, 4), np.nextafter(-pi, 0), np.nextafter(-pi, -4),
             np.nextafter(pi + tau, 0), np.nextafter(pi + tau, 10), np.nextafter(pi - tau, 0),
-            np.nextafter(pi - tau, -10), 1e-300, -1e-300, 5e-324, -5e-324, 1e-17, -1e-17,
+            np.nextafter(pi - tau, -10), pi - 2 * tau, -3 * pi, np.nextafter(pi - 2 * tau, 0),
+            np.nextafter(pi - 2 * tau, -20), 1e-300, -1e-300, 5e-324, -5e-324, 1e-17, -1e-17,
             1e6, -1e6, 1e300, -1e300, np.inf, -np.inf, np.nan]
     rng = np.random.default_rng(0)
     x = np.concatenate([edge, rng.uniform(-4, 4, 20000), rng.uniform(-40, 40, 20000),
