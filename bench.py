@@ -1,28 +1,38 @@
 #!/usr/bin/env python
-"""PI²-RH control-step benchmark (BASELINE.json metric: rollout-steps/s = K x T LWPR predicts).
+"""PI²-RH control-step benchmark (BASELINE.json metric: rollout-steps/s = K x T LWPR predicts,
+and control-step latency p50 at 1/2/4/8 B200).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 A step is one receding-horizon control step with iterations_per_step=1 on the
-named workload (default C2: K=65536 rollouts, T=50, L=100 receptive fields per
-axis, M=4 sub-rollouts — "uncertainty penalty on"), synthetic
-hybrid-LWPR model (paper_1503_00330_b200.synthetic), device-generated noise.
+named workload (default C2 = BASELINE configs[1]: K=65536 rollouts, T=50, L=100
+receptive fields per axis, M=4 sub-rollouts — "uncertainty penalty on", SURVEY.md
+§0.6), synthetic hybrid-LWPR model (paper_1503_00330_b200.synthetic),
+device-generated noise.
 
-* value: K*T*steps / device time of `steps` back-to-back iterations whose state,
-  plan and model are already resident in HBM (CUDA events on the launch stream,
+* value: K*T*steps / device time of `steps` back-to-back graph-replayed steps whose
+  state, plan and model are resident in HBM (CUDA events on the launch stream,
   barrier + synchronize on both sides, max over ranks).
-* e2e: the same metric through the public API `receding_horizon_step(...)`
-  with host state/plan in and host control/plan out (H2D + D2H inside).
-* roofline: the LWPR kernel (dominant) — algorithmic FP32 FLOPs per launch over
-  its CUDA-event duration vs the FP32 CUDA-core peak.
-* cpu_baseline / --impl reference: the reference algorithm (numpy oracle port,
-  oracle/) on the host cores, on a bounded sample of the same workload.
+* e2e: the same metric through the public API — `receding_horizon_step(...)` at
+  N=1, `distributed.ShardedEngine.optimize` at N>1 — host state/plan in, host
+  control/plan out (H2D + D2H inside the timed region).
+* roofline: the LWPR kernel (dominant): algorithmic 2^x per second over its
+  CUDA-event duration against the measured MUFU ex2 peak.
+* north_star: BASELINE C4 (K=2^20, T=50, L=100, M=1) on the same GPUs (strong
+  scaling): device ms/step, e2e p50/p99 against the 20 ms budget, the closed-loop
+  trial of the reference's own run_trial with this engine dropped in (N=1), and
+  at N>1 the speed-up over the same step on one GPU measured in the same run.
+* noise_stream: the host-noise path's exploration / dynamics noise streams
+  (controller.py:112-139) read by the attitude / rollout kernels, in GB/s.
+* cpu_baseline / --impl reference: the reference's own CPU implementation
+  (`pimpc` installed in baseline/_ref; the numpy oracle port if it is absent) on
+  the host cores.  --impl reference runs the FULL configured K.
 
-Under torchrun (N > 1) rollouts are sharded across ranks and the per-timestep
-softmax partials are all-gathered over NCCL.  Default --scaling weak: every GPU
-keeps the named workload's K rollouts (K_total = K x N, the same control step
-with N times the samples at the same latency); --scaling strong splits the
-named K over the N GPUs (BASELINE C4's framing: K=2^20 on 8 GPUs).
+N > 1: one process per GPU.  When WORLD_SIZE is unset, `--gpus N` re-launches
+itself under torch.distributed.run.  Rollouts are sharded across ranks (default
+--scaling strong: the named K split over the N GPUs; weak: K per GPU) and the
+per-timestep softmax partials are all-gathered over NCCL inside each rank's
+captured CUDA graph.
 """
 
 from __future__ import annotations
@@ -31,6 +41,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,6 +56,7 @@ import numpy as np  # noqa: E402
 METRIC = "rollout-steps/sec (K×T LWPR predicts)"
 UNIT = "rollout-steps/s"
 KERNELS_PER_ITER = 5  # attitude, lwpr, rollout, partials, combine
+BUDGET_MS = 20.0      # the receding-horizon real-time budget (north star)
 
 
 def parse():
@@ -54,17 +66,20 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="C2")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                   help="N > 1: weak = K rollouts per GPU, strong = K rollouts in total")
-    p.add_argument("--cpu-sample", type=int, default=4096, help="rollouts in the CPU baseline sample")
+    p.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                   help="N > 1: strong = the named K split over the GPUs, weak = K rollouts per GPU")
+    p.add_argument("--cpu-sample", type=int, default=4096, help="rollouts in the cpu_baseline sample")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--ref-budget-s", type=float, default=150.0,
+                   help="--impl reference: wall-clock budget of the timed steps (full K each)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--closed-loop-steps", type=int, default=200,
-                   help="control steps of the closed-loop trial (latency p50/p99); 0 disables")
+    p.add_argument("--no-north-star", action="store_true")
+    p.add_argument("--closed-loop-steps", type=int, default=500,
+                   help="north star: control steps of the closed-loop trial (BASELINE C4: 500); 0 disables")
     return p.parse_args()
 
 
-def workload(name: str):
+def workload(name: str, world: int, scaling: str):
     from paper_1503_00330_b200.synthetic import CONFIGS
 
     c = dict(CONFIGS[name])
@@ -75,51 +90,122 @@ def workload(name: str):
         "C4": "K=2^20, T=50, L=100, M=1 control step",
         "C5": "K=2^22, T=50, L=200, M=1",
     }[name]
-    return c, desc
+    if scaling == "weak":
+        c["K"] *= world
+        if world > 1:
+            desc += f" (x{world} GPUs, weak scaling: K per GPU)"
+    return c, f"{name}: {desc}"
+
+
+def config_dict(cfgd, desc):
+    """The `config` object of both arms' lines (identical for the same workload)."""
+    k = cfgd["K"]
+    return {"workload": desc, "K": k, "T": cfgd["T"], "L": cfgd["L"], "M": cfgd["M"], "iterations_per_step": 1,
+            "l2": "working set > L2: rows + LWPR planes + normals + costs = %.0f MB" % (k * cfgd["T"] * 64 / 1e6)}
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args) -> int:
+    """--gpus N without a launcher: one process per GPU under torch.distributed.run."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference(cfgd, sample_k: int, min_seconds: float, max_steps: int | None = None):
-    """Reference algorithm (oracle port) on the host cores: one optimisation iteration
-    (sample_noise [+ dyn] + evaluate + update) per step on a bounded sample."""
+class ThreadLocalCost:
+    """One reference RolloutCost per worker thread.  The reference's RolloutCost keeps
+    per-shape scratch buffers that its worker threads share (simworld.py:149-155, a race
+    when workers > 1); this harness-side proxy gives each thread its own."""
+
+    def __init__(self, ref, task, waypoint):
+        self.ref, self.task, self.waypoint, self._tl = ref, task, waypoint, threading.local()
+
+    def _cost(self):
+        c = getattr(self._tl, "c", None)
+        if c is None:
+            c = self._tl.c = self.ref.simworld.RolloutCost(self.task, self.waypoint)
+        return c
+
+    def crash_now(self, pos, out):
+        self._cost().crash_now(pos, out)
+
+    def stage_costs(self, pos, vel, ang, crashed, out):
+        self._cost().stage_costs(pos, vel, ang, crashed, out)
+
+
+def cpu_reference(cfgd, k, min_seconds=0.0, max_steps=None, budget_s=None):
+    """The reference's CPU implementation of one optimisation iteration (sample_noise
+    [+ dyn] + evaluate + update, controller.py:374-395) on K=k rollouts of the workload,
+    all host cores (thread pool over chunks, BLAS 1 thread).  pimpc itself when it is
+    installed (baseline/_ref), else the numpy oracle port (oracle/rollout.py)."""
     from threadpoolctl import threadpool_limits
 
     from oracle import rollout as RO
     from paper_1503_00330_b200 import synthetic
 
     T, L, M = cfgd["T"], cfgd["L"], cfgd["M"]
-    k = min(sample_k, cfgd["K"])
     workers = RO.default_workers()
     chunk = min(1024, -(-k // workers))
-    model = RO.Model(synthetic.hybrid_stacks(L, seed=0))
-    cost = RO.Cost(synthetic.DEFAULT_WAYPOINTS[1], synthetic.DEFAULT_OBSTACLES)
-    state = np.zeros(12)
-    state[0:3] = synthetic.DEFAULT_WAYPOINTS[0]
-    plan = np.tile([0.0, 0.0, 0.0, model.dyn.hover_thrust], (T, 1))
+    stacks = synthetic.hybrid_stacks(L, seed=0)
+    ref = synthetic.import_reference()
+    if ref is not None:
+        C = ref.controller
+        task = ref.simworld.Task.default()
+        model = synthetic.reference_hybrid(ref, stacks)
+        cfg = C.PiConfig(num_rollouts=k, sub_rollouts=M, horizon_steps=T, iterations_per_step=1, rng_seed=0,
+                         workers=workers, chunk_size=chunk)
+        cost = ThreadLocalCost(ref, task, 1) if workers > 1 else ref.simworld.RolloutCost(task, 1)
+        state = ref.dynamics.QuadState.hover(task.spawn)
+        plan = C.ControlPlan.hover(ref.dynamics.QuadParams(), T)
+        eng = C.RolloutEngine(model, cfg)
+
+        def one(cyc):
+            C.optimize(state, plan, cfg, model, cost, cyc, eng)
+        kind, what = "reference", "pimpc.controller.optimize (the reference package, baseline/_ref)"
+    else:
+        model = RO.Model(stacks)
+        cost = RO.Cost(synthetic.DEFAULT_WAYPOINTS[1], synthetic.DEFAULT_OBSTACLES)
+        state = np.zeros(12)
+        state[0:3] = synthetic.DEFAULT_WAYPOINTS[0]
+        plan = np.tile([0.0, 0.0, 0.0, model.dyn.hover_thrust], (T, 1))
+
+        def one(cyc):
+            RO.optimize(model, state, plan, cost, K=k, M=M, iterations=1, chunk=chunk, workers=workers, cycle=cyc)
+        kind, what = "port", "numpy oracle port of the reference (oracle/rollout.py; pimpc not installed)"
     times = []
     with threadpool_limits(1, "blas"):
-        RO.optimize(model, state, plan, cost, K=k, M=M, iterations=1, chunk=chunk, workers=workers)  # warm-up
+        one(10_000)  # warm-up (workspaces, thread pool)
         t_all = time.perf_counter()
         cyc = 0
         while True:
             t0 = time.perf_counter()
-            RO.optimize(model, state, plan, cost, K=k, M=M, iterations=1, chunk=chunk, workers=workers,
-                        cycle=cyc)
+            one(cyc)
             times.append(time.perf_counter() - t0)
             cyc += 1
+            el = time.perf_counter() - t_all
             if max_steps is not None and cyc >= max_steps:
                 break
-            if max_steps is None and (time.perf_counter() - t_all >= min_seconds and cyc >= 2):
+            if budget_s is not None and el + times[-1] > budget_s:
+                break
+            if max_steps is None and budget_s is None and el >= min_seconds and cyc >= 2:
                 break
     step = statistics.median(times)
     return {
         "value": k * T / step,
         "unit": UNIT,
         "cores": workers,
-        "kind": "port",
-        "sample": f"K={k} of {cfgd['K']} rollouts, T={T}, L={L}, M={M}; numpy oracle (oracle/rollout.py), "
-                  f"{workers} worker threads, BLAS 1 thread; median of {len(times)} steps "
-                  f"(noise + evaluate + update)",
+        "kind": kind,
+        "sample": f"K={k} of {cfgd['K']} rollouts, T={T}, L={L}, M={M}; {what}, {workers} worker threads, "
+                  f"BLAS 1 thread; median of {len(times)} steps (noise + evaluate + update)",
         "ms_per_step": step * 1e3,
         "step_times_s": times,
     }
@@ -247,128 +333,278 @@ def lwpr_traffic(config: str, tc: bool):
         return None
 
 
-def run_ours(args, rank: int, world: int, local: int):
+def pct(xs, q):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, max(0, math.ceil(q * len(xs)) - 1))]
+
+
+class Rig:
+    """One workload on this rank: the engine (one context at N=1, this rank's shard at
+    N>1), the device-resident step, and the public-API step with host buffers."""
+
+    def __init__(self, cfgd, world, local, stream, dist):
+        import paper_1503_00330_b200 as P
+        from paper_1503_00330_b200 import _abi, synthetic
+        from paper_1503_00330_b200.controller import dynamics_struct
+        from paper_1503_00330_b200.simworld import cost_struct
+
+        self.P, self._abi = P, _abi
+        self.cfgd, self.world, self.local, self.stream, self.dist = cfgd, world, local, stream, dist
+        K, T, L, M = cfgd["K"], cfgd["T"], cfgd["L"], cfgd["M"]
+        self.params = P.QuadParams()
+        self.model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=0), self.params)
+        self.task = P.Task.default()
+        self.cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=T, iterations_per_step=1, rng_seed=0)
+        self.state = P.QuadState.hover(self.task.spawn)
+        self.plan0 = P.ControlPlan.hover(self.params, T)
+        self.cost = P.RolloutCost(self.task, 1)
+        self.sptr = _abi.torch_stream(local)
+        if world > 1:
+            from paper_1503_00330_b200.distributed import ShardedEngine
+
+            self.eng = ShardedEngine(self.model, self.cfg, device=local)
+            self.ctx = self.eng.ctx
+            self.k_local = self.eng.stop - self.eng.start
+            self.eng.optimize(self.state, self.plan0, self.cost, 0)  # binds, stages, captures the graph
+        else:
+            self.eng = P.RolloutEngine(self.model, self.cfg, device=local, noise="device", use_graph=True)
+            self.ctx = self.eng.context(K, T)
+            self.k_local = K
+            self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, self.plan0.lo, self.plan0.hi))
+            self.ctx.call("pi2_set_cost", cost_struct(self.cost))
+            self.ctx.call("pi2_load_plan", _abi.ptr(self.state.as_array()),
+                          _abi.ptr(np.ascontiguousarray(self.plan0.controls)), self.sptr)
+
+    def device_step(self, cycle):
+        """One step on device-resident inputs (no host transfer, no synchronisation)."""
+        from paper_1503_00330_b200.controller import optimize_args
+
+        if self.world == 1:  # the whole iteration as one CUDA graph on the device-resident plan
+            self.ctx.call("pi2_iterate_device", optimize_args(self.cfg, cycle, use_graph=True), self.sptr)
+        else:  # this rank's captured step: pull, local kernels, NCCL all-gather, combine, push
+            self.eng.step_device()
+
+    def api_step(self, plan, cycle):
+        """receding_horizon_step through the public API with host state/plan."""
+        if self.world == 1:
+            return self.P.receding_horizon_step(self.state, plan, self.cfg, self.model, self.cost, cycle, self.eng)
+        opt = self.eng.optimize(self.state, plan, self.cost, cycle)
+        return opt.control_at(0), opt.shifted()
+
+    def barrier(self):
+        import torch
+
+        torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+
+        if self.dist is None:
+            return x
+        dev = f"cuda:{self.local}" if self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def time_device(self, steps, warmup, clocks=None):
+        """ms per step: `steps` back-to-back device steps, CUDA events on the launch stream,
+        barrier + synchronize on both sides, max over ranks."""
+        import torch
+
+        for w in range(warmup):
+            self.device_step(10_000 + w)
+        self.barrier()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if clocks is not None:
+            clocks.mark_start()
+        start.record(self.stream)
+        for s in range(steps):
+            self.device_step(s)
+        end.record(self.stream)
+        while not end.query():  # a sleeping wait keeps the GIL free for the clock sampler
+            time.sleep(0.0005)
+        self.barrier()
+        if clocks is not None:
+            clocks.mark_end()
+        return self.max_over_ranks(start.elapsed_time(end)) / steps
+
+    def time_api(self, steps, warmup):
+        """(total seconds, per-step latencies in ms) of the public-API step, max over ranks."""
+        for w in range(warmup):
+            self.api_step(self.plan0, 10_000 + w)
+        self.barrier()
+        plan, lat = self.plan0, []
+        for s in range(steps):
+            t0 = time.perf_counter()
+            _, plan = self.api_step(plan, s)
+            lat.append(time.perf_counter() - t0)
+        total = self.max_over_ranks(sum(lat))
+        lat_ms = [x * 1e3 for x in lat]
+        return total, {"p50": self.max_over_ranks(statistics.median(lat_ms)),
+                       "p99": self.max_over_ranks(pct(lat_ms, 0.99)), "max": self.max_over_ranks(max(lat_ms))}
+
+
+def noise_stream(rig, local):
+    """Host-noise path (controller.py:112-139: the reference's (K,N,4) f64 exploration and
+    (K,M,N,3) f32 dynamics noise, resident in HBM): bandwidth of the kernels that stream
+    them, from CUDA events around each kernel (pi2_profile_evaluate)."""
     import torch
 
-    import paper_1503_00330_b200 as P
-    from paper_1503_00330_b200 import _abi, synthetic
-    from paper_1503_00330_b200.controller import dynamics_struct, optimize_args
-    from paper_1503_00330_b200.simworld import cost_struct
+    _abi = rig._abi
+    K, T, M = rig.cfgd["K"], rig.cfgd["T"], rig.cfgd["M"]
+    dev = f"cuda:{local}"
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    eps = torch.randn((K, T, 4), dtype=torch.float64, device=dev, generator=g) * torch.tensor(
+        rig.cfg.exploration_std, dtype=torch.float64, device=dev)
+    dyn = torch.randn((K, M, T, 3), dtype=torch.float32, device=dev, generator=g) if M > 1 else None
+    ms = (_abi.C.c_double * 3)()
+    torch.cuda.synchronize()  # the noise tensors were written on torch's stream
+    rig.ctx.call("pi2_profile_evaluate", _abi.ptr(rig.state.as_array()), _abi.ptr(np.ascontiguousarray(rig.plan0.controls)),
+                 _abi.ptr(eps), _abi.ptr(dyn), 10, ms)
+    att, lw, roll = list(ms)
+    eps_b = K * T * 4 * 8
+    dyn_b = K * M * T * 3 * 4 if M > 1 else 0
+    peak = float(measured_peaks().get("hbm_gbs", 6547.2))
+    out = {"attitude_ms": att, "lwpr_ms": lw, "rollout_ms": roll,
+           "eps_bytes": eps_b, "eps_gbs": eps_b / (att * 1e-3) / 1e9,
+           # the attitude kernel also writes the (K*N) float4 LWPR rows and reads the plan
+           "attitude_kernel_gbs": (eps_b + K * T * 16) / (att * 1e-3) / 1e9,
+           "peak_gbs": peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+    out["eps_frac"] = out["eps_gbs"] / peak
+    out["attitude_kernel_frac"] = out["attitude_kernel_gbs"] / peak
+    if dyn_b:
+        out.update({"dyn_bytes": dyn_b, "dyn_gbs": dyn_b / (roll * 1e-3) / 1e9,
+                    "combined_gbs": (eps_b + dyn_b) / ((att + roll) * 1e-3) / 1e9})
+        out["combined_frac"] = out["combined_gbs"] / peak
+    out["what"] = ("algorithmic noise bytes / CUDA-event time of the kernel that streams them (attitude: "
+                   "exploration noise; rollout/cost: dynamics noise); the rollout kernel is issue-bound, "
+                   "so its rate is not a bandwidth ceiling")
+    del eps, dyn
+    return out
+
+
+def closed_loop(cfgd, local, steps):
+    """BASELINE C4's closed loop: the reference's own run_trial (simworld.py:270-380:
+    plant, waypoints, crash verdicts, K=1 plan-cost probe) with this engine dropped in
+    (device noise, one CUDA graph per control step); latency of every
+    receding_horizon_step call, host state in, control out."""
+    from paper_1503_00330_b200 import dropin, synthetic
+
+    ref = synthetic.import_reference()
+    if ref is None:
+        return {"skipped": "reference package pimpc not installed (baseline/_ref)"}
+    p = ref.dynamics.QuadParams()
+    model = synthetic.reference_hybrid(ref, synthetic.hybrid_stacks(cfgd["L"], seed=0), p)
+    gt = ref.dynamics.PerturbedModel(p, drag_coeff=0.08, thrust_scale=0.97)
+    cfg = ref.controller.PiConfig(num_rollouts=cfgd["K"], sub_rollouts=cfgd["M"], horizon_steps=cfgd["T"],
+                                  iterations_per_step=1)
+    lat = []
+    with dropin.patched(ref.controller, noise="device", device=local, step_times=lat):
+        t0 = time.perf_counter()
+        trial = ref.simworld.run_trial(ref.simworld.Task.default(), cfg, model, gt, seed=0, step_cap=steps)
+        wall = time.perf_counter() - t0
+    raw = np.asarray(lat) * 1e3
+    tl = sorted(raw[1:]) if len(raw) > 1 else sorted(raw)  # steady state: after the setup step
+    return {
+        "what": "pimpc.simworld.run_trial (the reference's closed loop) with paper_1503_00330_b200.RolloutEngine "
+                "dropped in (dropin.patched, device noise); plant = pimpc PerturbedModel(drag 0.08, thrust x0.97)",
+        "steps": int(trial.steps), "outcome": trial.outcome,
+        "p50_ms": float(np.median(tl)), "p99_ms": float(pct(tl, 0.99)), "max_ms": float(tl[-1]),
+        "budget_ms": BUDGET_MS, "within_budget": bool(tl[-1] < BUDGET_MS),
+        "first_step_ms": float(raw[0]) if len(raw) else None,
+        "first_step": "context creation, weight staging and CUDA graph capture; p50/p99/max cover the later steps",
+        "trial_wall_s": wall,
+    }
+
+
+def north_star(args, world, local, stream, dist, rank):
+    """BASELINE C4 (K=2^20, T=50, L=100, M=1): one step split over the N GPUs."""
+    import torch
+
+    cfgd, desc = workload("C4", world, "strong")
+    rig = Rig(cfgd, world, local, stream, dist)
+    steps = max(5, min(args.steps, 20))
+    ms = rig.time_device(steps, max(3, min(args.warmup, 5)))
+    _, lat = rig.time_api(steps, 3)
+    out = {"workload": desc, "K": cfgd["K"], "K_per_gpu": rig.k_local, "n_gpus": world, "scaling": "strong",
+           "device_ms_per_step": ms, "value": cfgd["K"] * cfgd["T"] / (ms * 1e-3), "unit": UNIT,
+           "e2e_ms": lat, "budget_ms": BUDGET_MS, "within_budget": bool(lat["p99"] < BUDGET_MS),
+           "api": "receding_horizon_step" if world == 1 else "distributed.ShardedEngine.optimize (graph-captured)"}
+    del rig
+    torch.cuda.empty_cache()
+    if world > 1:  # the same step on one GPU, same run: the strong-scaling speed-up
+        one_ms = None
+        if rank == 0:
+            solo = Rig(cfgd, 1, local, stream, None)
+            one_ms = solo.time_device(steps, 3)
+            del solo
+            torch.cuda.empty_cache()
+        dist.barrier()
+        if rank == 0:
+            out["one_gpu_ms_per_step"] = one_ms
+            out["speedup_vs_1gpu"] = one_ms / ms
+            out["strong_scaling_efficiency"] = one_ms / ms / world
+    elif args.closed_loop_steps > 0:
+        out["closed_loop"] = closed_loop(cfgd, local, args.closed_loop_steps)
+    return out
+
+
+def run_ours(args, rank: int, world: int, local: int):
+    import torch
 
     dist = None
     # one rank per GPU; PI2_DIST_BACKEND=gloo lets several ranks share a GPU to
     # exercise the multi-rank path where only one GPU exists (timings meaningless)
     backend = os.environ.get("PI2_DIST_BACKEND", "nccl")
     local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    torch.cuda.set_device(local)
-    cfgd, desc = workload(args.config)
-    if args.scaling == "weak":
-        cfgd["K"] *= world
+    cfgd, desc = workload(args.config, world, args.scaling)
     K, T, L, M = cfgd["K"], cfgd["T"], cfgd["L"], cfgd["M"]
-    params = P.QuadParams()
-    model = P.HybridModel.from_stacks(synthetic.hybrid_stacks(L, seed=0), params)
-    task = P.Task.default()
-    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=T, iterations_per_step=1, rng_seed=0)
-    state = P.QuadState.hover(task.spawn)
-    plan0 = P.ControlPlan.hover(params, T)
-    cost = P.RolloutCost(task, 1)
     stream = torch.cuda.Stream(device=local)  # dedicated stream: kernels, events and NCCL share it
     torch.cuda.set_stream(stream)
-    sptr = _abi.torch_stream(local)
-
-    if world > 1:
-        from paper_1503_00330_b200.distributed import ShardedEngine, gather_partials
-
-        eng = ShardedEngine(model, cfg, device=local)
-        ctx = eng.ctx
-        k_local = eng.stop - eng.start
-    else:
-        eng = P.RolloutEngine(model, cfg, device=local, noise="device", use_graph=True)
-        ctx = eng.context(K, T)
-        k_local = K
-    ctx.call("pi2_set_dynamics", dynamics_struct(params, plan0.lo, plan0.hi))
-    ctx.call("pi2_set_cost", cost_struct(cost))
-    ctx.call("pi2_load_plan", _abi.ptr(state.as_array()), _abi.ptr(np.ascontiguousarray(plan0.controls)), sptr)
-    partial = torch.empty((T, _abi.PARTIAL_WIDTH), dtype=torch.float64, device=f"cuda:{local}")
-
-    def device_step(cycle):
-        if world == 1:  # the whole iteration as one CUDA graph on the device-resident plan
-            ctx.call("pi2_iterate_device", optimize_args(cfg, cycle, use_graph=True), sptr)
-            return
-        a = optimize_args(cfg, cycle, use_graph=False)
-        ctx.call("pi2_iterate_local", a, 0, _abi.ptr(partial), sptr)
-        g = gather_partials(partial)
-        ctx.call("pi2_iterate_finalize", _abi.ptr(g), world, float(cfg.temperature), sptr)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    rig = Rig(cfgd, world, local, stream, dist)
+    _abi = rig._abi
 
     # ---- device-resident throughput (value)
-    for w in range(args.warmup):
-        device_step(10_000 + w)
-    barrier()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        clocks.mark_start()
-        start.record(stream)
-        for s in range(args.steps):
-            device_step(s)
-        end.record(stream)
-        while not end.query():  # a sleeping wait keeps the GIL free for the clock sampler
-            time.sleep(0.0005)
-        barrier()
-        clocks.mark_end()
-    dev_ms = max_over_ranks(start.elapsed_time(end))
-    ms_per_step = dev_ms / args.steps
-    value = K * T * args.steps / (dev_ms / 1e3)
+        ms_per_step = rig.time_device(args.steps, args.warmup, clocks)
+    value = K * T / (ms_per_step * 1e-3)
 
     # ---- stage profile (dominant kernel = LWPR), CUDA events on the context stream
+    from paper_1503_00330_b200.controller import optimize_args
+
     stage_ms = (_abi.C.c_double * 5)()
-    ctx.call("pi2_profile_iteration", optimize_args(cfg, 0, use_graph=False), 10, stage_ms)
+    rig.ctx.call("pi2_profile_iteration", optimize_args(rig.cfg, 0, use_graph=False), 10, stage_ms)
     stages = dict(zip(["attitude", "lwpr", "rollout_cost", "partials", "combine"], list(stage_ms)))
+    # which LWPR kernel ran, and the share of its 2^x on MUFU (the rest on the FMA pipe)
+    kern, share = _abi.C.c_int32(), _abi.C.c_double()
+    rig.ctx.call("pi2_lwpr_kernel", int(M > 1), _abi.C.byref(kern), _abi.C.byref(share))
 
     # ---- end to end through the public API (host state/plan in, control/plan out)
-    plan = plan0
-    lat = []
-    if world > 1:
-        for w in range(args.warmup):
-            eng.optimize(state, plan, cost, 10_000 + w)
-        barrier()
-        for s in range(args.steps):
-            t0 = time.perf_counter()
-            opt = eng.optimize(state, plan, cost, s)
-            ctrl, plan = opt.control_at(0), opt.shifted()
-            lat.append(time.perf_counter() - t0)
-    else:
-        for w in range(args.warmup):
-            P.receding_horizon_step(state, plan0, cfg, model, cost, 10_000 + w, eng)
-        barrier()
-        for s in range(args.steps):
-            t0 = time.perf_counter()
-            ctrl, plan = P.receding_horizon_step(state, plan, cfg, model, cost, s, eng)
-            lat.append(time.perf_counter() - t0)
-    e2e_s = max_over_ranks(sum(lat))
-    lat_ms = sorted(x * 1e3 for x in lat)
-    p50 = max_over_ranks(statistics.median(lat_ms))
-    p99 = max_over_ranks(lat_ms[min(len(lat_ms) - 1, math.ceil(0.99 * len(lat_ms)) - 1)])
+    e2e_s, lat = rig.time_api(args.steps, args.warmup)
+
+    # ---- noise-stream bandwidth of the host-noise path (N=1)
+    ns = noise_stream(rig, local) if world == 1 else None
+
+    k_local = rig.k_local
+    del rig
+    torch.cuda.empty_cache()
+    ns_obj = None
+    if not args.no_north_star:
+        ns_obj = north_star(args, world, local, stream, dist, rank)
 
     if rank != 0:
         return None
@@ -380,15 +616,11 @@ def run_ours(args, rank: int, world: int, local: int):
     rows = k_local * T
     flops_per_field = 32 if M > 1 else 27  # 27 (+5 variance) per (row, axis, field)
     lwpr_flops = rows * 3 * L * flops_per_field
-    achieved = lwpr_flops / (stages["lwpr"] / 1e3) / 1e12
-    # which LWPR kernel ran: the tcgen05 one for the variance path unless disabled
-    # which LWPR kernel ran, and the share of its 2^x on MUFU (the rest on the FMA pipe)
-    kern, share = _abi.C.c_int32(), _abi.C.c_double()
-    ctx.call("pi2_lwpr_kernel", int(M > 1), _abi.C.byref(kern), _abi.C.byref(share))
-    tc = kern.value == 1
-    exps = rows * 3 * L  # one 2^x per (row, axis, field)
-    mufu_peak = float(peaks.get("mufu_ex2_per_s", 4.60e12))
     lw_s = stages["lwpr"] / 1e3
+    achieved = lwpr_flops / lw_s / 1e12
+    tc = kern.value == 1
+    exps = rows * 3 * L  # one 2^x per (row, axis, field): the algorithmic count
+    mufu_peak = float(peaks.get("mufu_ex2_per_s", 4.60e12))
     clk = clocks.summary()
     peak_obs = n_sm * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12 if clk.get("sm_mhz") else None
     h2d = 12 * 8 + T * 4 * 8 + 8 * (12 + 4 * 16 + 4 + 2) + 4 * 48  # state + plan + StepArgs
@@ -399,20 +631,23 @@ def run_ours(args, rank: int, world: int, local: int):
         "frac_at_observed_clock": (achieved / peak_obs) if peak_obs else None,
         "flops_per_launch": lwpr_flops, "flops_per_field": flops_per_field,
     }
-    mufu = {"ex2_per_launch": exps, "mufu_share": share.value,
-            "achieved": exps * share.value / lw_s / 1e12, "peak": mufu_peak / 1e12, "unit": "Tex2/s",
-            "frac": exps * share.value / lw_s / mufu_peak,
-            "peak_source": "profiles/micro/mufu_mix_b200.txt (MUFU-only ex2 stream, 148 SMs)"}
-    if tc:  # binding unit: MUFU (the linear parts are on the tensor cores)
+    ex_rate = exps / lw_s
+    if tc:  # binding unit: the exponentials (the linear parts are on the tensor cores)
         roofline = {"bound": "mufu", "kernel": "lwpr_tc_kernel (tcgen05 3xTF32 field GEMM + exp/moments)",
-                    **{k: mufu[k] for k in ("achieved", "peak", "unit", "frac", "peak_source")},
+                    "achieved": ex_rate / 1e12, "peak": mufu_peak / 1e12, "unit": "Tex2/s",
+                    "frac": ex_rate / mufu_peak,
+                    "peak_source": "profiles/micro/mufu_mix_b200.txt (MUFU-only ex2 stream, 148 SMs)",
+                    "what": "algorithmic 2^x per launch (rows x 3 axes x L fields) / CUDA-event duration; a share "
+                            "runs as a polynomial on the FMA pipe (mufu_share on MUFU)",
                     "ex2_per_launch": exps, "mufu_share": share.value,
+                    "mufu_busy_frac": ex_rate * share.value / mufu_peak,
                     "traffic": lwpr_traffic(args.config, tc) if world == 1 else None,
                     "fp32_equivalent": {**fp32, "note": "the same algorithmic FLOPs against the FP32 CUDA-core "
                                         "peak; above 1 when the tensor cores carry the linear parts"}}
     else:
         roofline = {"bound": "fp32", "kernel": "lwpr_kernel (CUDA cores, FFMA2)", **fp32,
-                    "traffic": lwpr_traffic(args.config, tc) if world == 1 else None, "mufu": mufu}
+                    "traffic": lwpr_traffic(args.config, tc) if world == 1 else None,
+                    "mufu": {"achieved": ex_rate / 1e12, "peak": mufu_peak / 1e12, "unit": "Tex2/s"}}
     line = {
         "metric": METRIC,
         "value": value,
@@ -427,14 +662,10 @@ def run_ours(args, rank: int, world: int, local: int):
         "dtype": "f32 (LWPR: linear parts as 3xTF32 tcgen05 products with f32 accumulation, exp/moments f32; "
                  "integration, cost) + f64 (attitude, cost-to-go, update)",
         "data": "synthetic (seeded hybrid-LWPR model linearising the rigid-body quadrotor; device Philox noise)",
-        "config": {
-            "workload": f"{args.config}: {desc}" + (f" (x{world} GPUs, weak scaling: K per GPU)"
-                                                    if world > 1 and args.scaling == "weak" else ""),
-            "K": K, "K_per_gpu": k_local, "T": T, "L": L, "M": M, "iterations_per_step": 1,
-            "parallelism": f"rollouts sharded over {world} GPU(s)",
-            "l2": "working set > L2 (xin + LWPR planes + exploration normals + costs ≈ %.0f MB per GPU)"
-                  % ((k_local * T * (16 + 24 + 16 + 8)) / 1e6),
-        },
+        "config": config_dict(cfgd, desc),
+        "sharding": {"K_per_gpu": k_local, "parallelism": f"rollouts sharded over {world} GPU(s)"
+                     + ("" if world == 1 else "; NCCL all-gather of per-timestep softmax partials inside each "
+                        "rank's captured CUDA graph")},
         "e2e": {
             "value": K * T * args.steps / e2e_s,
             "unit": UNIT,
@@ -443,29 +674,18 @@ def run_ours(args, rank: int, world: int, local: int):
             "api": "paper_1503_00330_b200.receding_horizon_step(noise='device' engine)" if world == 1
                    else "distributed.ShardedEngine.optimize",
         },
-        "latency_ms": {"p50": p50, "p99": p99, "what": "e2e control step (host state/plan -> control)"},
+        "latency_ms": {**lat, "what": "e2e control step (host state/plan -> control)"},
         "roofline": roofline,
         "stages_ms": stages,
         "clocks": clk,
-        "gpu_launches": args.steps * (KERNELS_PER_ITER + (1 if world > 1 else 0)),
+        "gpu_launches": args.steps * (KERNELS_PER_ITER + (2 if world > 1 else 0)),
     }
-    if world == 1 and args.closed_loop_steps > 0:
-        gt = P.PerturbedModel(params, drag_coeff=0.08, thrust_scale=0.97)
-        trial = P.run_trial(task, P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=T, iterations_per_step=1),
-                            model, gt, seed=0, step_cap=args.closed_loop_steps, noise="device", device=local)
-        raw = np.asarray(trial.step_latency_s) * 1e3
-        tl = np.sort(raw[1:]) if len(raw) > 1 else np.sort(raw)  # steady state: after the setup step
-        line["closed_loop"] = {
-            "what": "simworld.run_trial with device noise: latency of each receding_horizon_step (host state in, "
-                    "control out); plant = PerturbedModel(drag 0.08, thrust x0.97)",
-            "steps": int(trial.steps), "outcome": trial.outcome,
-            "p50_ms": float(np.median(tl)), "p99_ms": float(tl[min(len(tl) - 1, math.ceil(0.99 * len(tl)) - 1)]),
-            "max_ms": float(tl[-1]), "budget_ms": 20.0,
-            "first_step_ms": float(raw[0]) if len(raw) else None,
-            "first_step": "context creation, weight staging and CUDA graph capture; p50/p99/max cover the later steps",
-        }
+    if ns is not None:
+        line["noise_stream"] = ns
+    if ns_obj is not None:
+        line["north_star"] = ns_obj
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(cfgd, args.cpu_sample, args.cpu_seconds)
+        cb = cpu_reference(cfgd, min(args.cpu_sample, K), min_seconds=args.cpu_seconds)
         cb.pop("step_times_s", None)
         cb["cpu_model"] = cpu_model()
         line["cpu_baseline"] = cb
@@ -473,36 +693,42 @@ def run_ours(args, rank: int, world: int, local: int):
 
 
 def run_reference(args, world: int = 1):
-    cfgd, desc = workload(args.config)
-    if args.scaling == "weak":
-        cfgd["K"] *= world  # the same config as our arm; the CPU sample below is bounded anyway
-    cb = cpu_reference(cfgd, args.cpu_sample, 0.0, max_steps=args.warmup + args.steps)
-    times = cb.pop("step_times_s")[args.warmup:] or [cb["ms_per_step"] / 1e3]
-    step = sum(times) / len(times)
-    k = min(args.cpu_sample, cfgd["K"])
-    value = k * cfgd["T"] / step
+    """The reference arm: the reference's own CPU path on the FULL configured workload
+    (same config object as our arm), on the host cores; the number of timed steps is
+    bounded by --ref-budget-s (each step is a whole iteration at full K)."""
+    cfgd, desc = workload(args.config, world, args.scaling)
+    cb = cpu_reference(cfgd, cfgd["K"], max_steps=args.warmup + args.steps, budget_s=args.ref_budget_s)
+    times = cb.pop("step_times_s")
+    timed = times[args.warmup:] if len(times) > args.warmup else times[-max(1, len(times) // 2):]
+    step = sum(timed) / len(timed)
+    value = cfgd["K"] * cfgd["T"] / step
     return {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
         "n_gpus": 0,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": len(timed),
+        "warmup": len(times) - len(timed) + 1,
+        "steps_requested": args.steps,
         "ms_per_step": step * 1e3,
         "higher_is_better": True,
         "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f32 + f64 (numpy)",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {desc}", **cfgd, "iterations_per_step": 1},
-        "cpu_baseline": {**cb, "value": value, "cpu_model": cpu_model()},
+        "config": config_dict(cfgd, desc),
+        "cpu_baseline": {**cb, "value": value, "cpu_model": cpu_model(),
+                         "sample": cb["sample"] + f"; {len(timed)} timed steps within a {args.ref_budget_s:.0f} s "
+                                                  "budget"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

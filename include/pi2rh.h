@@ -217,6 +217,13 @@ int64_t pi2_partial_chunk(void); /* rollouts per leaf partial */
  * averaged over `reps` (plan not updated).  stage_ms[5] = attitude, LWPR,
  * rollout/cost, partials, combine (ms). */
 int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms);
+/* Stage timing of the host-noise evaluate path (pi2_evaluate_device on DEVICE
+ * copies of the reference's noise streams, controller.py:112-139, 197-247):
+ * stage_ms[3] = attitude (reads the (K,N,4) f64 exploration noise), LWPR,
+ * rollout/cost (reads the (K,M,N,3) f32 dynamics noise when M > 1), averaged
+ * over `reps`.  Benchmark introspection: the noise-stream HBM bandwidth. */
+int pi2_profile_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise_dev,
+                         const float *dyn_dev, int32_t reps, double *stage_ms);
 /* Which LWPR kernel the rollout path of this context runs for the staged
  * model (variance != 0: the sub-rollout path with standard deviations):
  * *kernel_out = PI2_LWPR_CUDA_CORES or PI2_LWPR_TENSOR_CORES; *mufu_share

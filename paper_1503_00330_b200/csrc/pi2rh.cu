@@ -1092,6 +1092,39 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
   return PI2_OK;
 }
 
+int pi2_profile_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise_dev,
+                         const float *dyn_dev, int32_t reps, double *stage_ms) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  if (!state || !plan || !noise_dev || reps < 1 || !stage_ms) return fail(ctx, PI2_ERR_INVALID, "bad argument");
+  if (spread(ctx) && !dyn_dev)
+    return fail(ctx, PI2_ERR_INVALID, "probabilistic model with sub_rollouts > 1 needs dyn_noise");
+  cudaStream_t st = ctx->stream;
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, state, nullptr, 1e8, st));
+  TRY(stage_plan(ctx, plan, st));
+  cudaEvent_t ev[4];
+  for (auto &e : ev) CU(cudaEventCreate(&e));
+  double acc[3] = {0, 0, 0};
+  int rc = PI2_OK;
+  for (int r = 0; r < reps && rc == PI2_OK; ++r) {
+    cudaEventRecord(ev[0], st);
+    rc = launch_rollouts(ctx, 0, noise_dev, dyn_dev, ctx->d_costs, ctx->d_crash, st, ev);
+    if (rc != PI2_OK) break;
+    cudaEventRecord(ev[3], st);
+    if (cudaEventSynchronize(ev[3]) != cudaSuccess) rc = fail(ctx, PI2_ERR_CUDA, "profile: %s", cudaGetErrorString(cudaGetLastError()));
+    for (int i = 0; i < 3 && rc == PI2_OK; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      acc[i] += ms;
+    }
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  TRY(rc);
+  for (int i = 0; i < 3; ++i) stage_ms[i] = acc[i] / reps;
+  return PI2_OK;
+}
+
 int pi2_iterate_finalize(pi2_ctx *ctx, const double *gathered, int32_t world, double temperature,
                          void *stream) {
   if (!ctx || !gathered || world < 1) return fail(ctx, PI2_ERR_INVALID, "bad gathered partials");

@@ -152,16 +152,10 @@ class ShardedEngine:
         self.graph_captures += 1
         return g
 
-    def optimize(self, state, plan: ControlPlan, cost_model, cycle_index: int = 0) -> ControlPlan:
+    def step_device(self) -> None:
+        """The staged step's device work on torch's current stream (the captured graph's
+        replay with NCCL; eager otherwise); the plan lands in the pinned block."""
         cfg = self.config
-        if cfg.iterations_per_step == 0:
-            return plan
-        self._bind(plan, cost_model)
-        args = optimize_args(cfg, cycle_index, use_graph=self.use_graph)
-        st = self._state_buf
-        st[0:3], st[3:6], st[6:9], st[9:12] = state.position, state.velocity, state.angles, state.rates
-        self._plan_buf[...] = plan.controls
-        self.ctx.call("pi2_stage_step", _abi.ptr(st), _abi.ptr(self._plan_buf), args)
         stream = _abi.torch_stream(self.device)
         temperature = float(cfg.temperature)
         if self.use_graph:
@@ -178,6 +172,18 @@ class ShardedEngine:
                 gathered = gather_partials(self.partial, self.group)
                 self.ctx.call("pi2_iterate_finalize", _abi.ptr(gathered), self.world, temperature, stream)
             self.ctx.call("pi2_enqueue_push", stream)
+
+    def optimize(self, state, plan: ControlPlan, cost_model, cycle_index: int = 0) -> ControlPlan:
+        cfg = self.config
+        if cfg.iterations_per_step == 0:
+            return plan
+        self._bind(plan, cost_model)
+        args = optimize_args(cfg, cycle_index, use_graph=self.use_graph)
+        st = self._state_buf
+        st[0:3], st[3:6], st[6:9], st[9:12] = state.position, state.velocity, state.angles, state.rates
+        self._plan_buf[...] = plan.controls
+        self.ctx.call("pi2_stage_step", _abi.ptr(st), _abi.ptr(self._plan_buf), args)
+        self.step_device()
         out = np.empty_like(self._plan_buf)
-        self.ctx.call("pi2_fetch_plan", _abi.ptr(out), stream)
+        self.ctx.call("pi2_fetch_plan", _abi.ptr(out), _abi.torch_stream(self.device))
         return plan.replaced(out)
