@@ -145,6 +145,13 @@ int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan,
                         const double *noise_dev, const float *dyn_noise_dev, double cost_ceiling,
                         double *costs_dev, uint8_t *crash_dev, void *stream);
 
+/* RolloutEngine.evaluate on the DEVICE noise streams of (seed, cycle,
+ * iteration) that pi2_optimize draws (the same kernels as one optimisation
+ * iteration, without the update): costs (K,N) and crash flags (K,) to DEVICE
+ * buffers.  The noise itself is pi2_device_noise's output. */
+int pi2_evaluate_device_noise(pi2_ctx *ctx, const double *state, const double *plan,
+                              const pi2_optimize_args *args, int32_t iteration, double *costs_dev,
+                              uint8_t *crash_dev, void *stream);
 /* path_integral_update (controller.py:356-371) for an arbitrary batch:
  * per-timestep min-shifted softmax of -costs/temperature, weighted noise sum,
  * clip to the plan bounds.  HOST buffers; K may differ from the context's. */

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "pi2_set_cost": (C.c_int, [_P, C.POINTER(Cost)]),
     "pi2_evaluate": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, _P, _P]),
     "pi2_evaluate_device": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
+    "pi2_evaluate_device_noise": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs), C.c_int32, _P, _P, _P]),
     "pi2_update": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_double, _P]),
     "pi2_update_device": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P, C.c_double, _P, _P]),
     "pi2_optimize": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs)]),

@@ -798,6 +798,23 @@ int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan, c
   return PI2_OK;
 }
 
+int pi2_evaluate_device_noise(pi2_ctx *ctx, const double *state, const double *plan, const pi2_optimize_args *args,
+                              int32_t iteration, double *costs_dev, uint8_t *crash_dev, void *stream) {
+  TRY(check_ready(ctx));
+  TRY(bind(ctx));
+  TRY(validate_opt(ctx, args));
+  if (!state || !plan || !costs_dev || !crash_dev || iteration < 0) return fail(ctx, PI2_ERR_INVALID, "bad argument");
+  cudaStream_t st = pick(ctx, stream);
+  TRY(ensure_params(ctx));
+  TRY(stage_args(ctx, state, args, args->cost_ceiling, st));
+  TRY(stage_plan(ctx, plan, st));
+  TRY(launch_rollouts(ctx, iteration, nullptr, nullptr, ctx->d_costs, crash_dev, st));
+  const dim3 tg((unsigned)((ctx->K + 31) / 32), (unsigned)((ctx->N + 31) / 32));
+  transpose_costs_kernel<<<tg, dim3(32, 8), 0, st>>>(ctx->d_costs, costs_dev, ctx->K, ctx->N);
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
 int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise,
                  const float *dyn, double ceiling, double *costs_out, uint8_t *crash_out) {
   TRY(check_ready(ctx));

@@ -388,43 +388,6 @@ def test_device_optimize_beyond_sixteen_iterations(use_graph):
     np.testing.assert_array_equal(fused.controls, p.controls)
 
 
-@pytest.mark.parametrize("K,N,L,M", [(65536, 50, 100, 4),      # C2
-                                     (262144, 100, 1000, 1),   # C3: streamed weights
-                                     (1 << 20, 50, 100, 1)])   # C4 (one GPU)
-def test_full_size_baseline_configs_device_path(K, N, L, M):
-    """BASELINE configs at full size through the real-time path (device noise, one CUDA
-    graph, tensor-core LWPR): the fused update equals evaluate + update on the
-    materialised noise bitwise; costs and crash flags of 512 sampled rollouts match the
-    oracle; the full-size update matches the oracle's update of the same costs."""
-    stacks = synthetic.hybrid_stacks(L, seed=0)
-    params = P.QuadParams()
-    model = P.HybridModel.from_stacks(stacks, params)
-    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=0)
-    task = P.Task.default()
-    state, plan, cost = P.QuadState.hover(task.spawn), P.ControlPlan.hover(params, N), P.RolloutCost(task, 1)
-    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
-    fused = eng.optimize_device(state, plan, cost, cycle_index=3)
-    ctx = eng.context(K, N)
-    eps = np.empty((K, N, 4))
-    ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, cfg.rng_seed, 3, 0, _abi.ptr(cfg.exploration_std), _abi.ptr(eps))
-    dyn = None
-    if M > 1:
-        dyn = np.empty((K, M, N, 3), np.float32)
-        ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, cfg.rng_seed, 3, 0, None, _abi.ptr(dyn))
-    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, eps, cost, dyn)
-    np.testing.assert_array_equal(fused.controls, P.path_integral_update(plan, b, cfg.temperature).controls)
-    assert 0 < b.crash_flags.sum() < K  # the workload has both outcomes
-    om = RO.Model(stacks)
-    lo, hi = om.dyn.bounds()
-    pick = np.sort(np.random.default_rng(5).choice(K, 512, replace=False))
-    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, eps[pick],
-                         RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES), None if dyn is None else dyn[pick], M)
-    np.testing.assert_array_equal(b.crash_flags[pick], rf)
-    assert cost_rel_err(b.costs_to_go[pick], rc) < COST_RTOL
-    ref_update = RO.update(plan.controls, lo, hi, b.costs_to_go, eps, cfg.temperature)
-    assert np.all(du_err(fused.controls, ref_update, plan.controls) < DU_TOL)
-
-
 @pytest.mark.parametrize("K,N,L,M", [(1, 1, 1, 1), (1, 5, 3, 4), (257, 1, 8, 3), (8192, 3, 16, 1),
                                      (8193, 3, 16, 1), (8193, 2, 16, 4), (300, 7, 130, 2)])
 def test_device_path_edge_shapes(K, N, L, M):
