@@ -280,9 +280,10 @@ __device__ __forceinline__ float exact_weight(const float *f, const float4 &x, f
   return e;
 }
 
+// (mean, variance) by value: output pointers to a non-inlined function would put the
+// callers' mean/var in local memory on their fast path too
 template <int LAY>
-__device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, float qrow, float gx,
-                                            float *mean_out, float *var_out) {
+__device__ __noinline__ float2 lwpr_row_exact(const float *rec, int nf, float4 x, float qrow, float gx) {
   constexpr int RS = Lay<LAY>::RS;
   float den = 0.0f;
   for (int l = 0; l < nf; ++l) den = __fadd_rn(den, exact_weight<LAY>(rec + (int64_t)l * RS, x, qrow));
@@ -299,8 +300,7 @@ __device__ __noinline__ void lwpr_row_exact(const float *rec, int nf, float4 x, 
     const float d = __fsub_rn(mean, __fadd_rn(field_local<LAY>(f, x), gx));
     var = __fadd_rn(var, __fmul_rn(w, __fadd_rn(__fmul_rn(d, d), field_lvar<LAY>(f))));
   }
-  *mean_out = mean;
-  *var_out = var;
+  return make_float2(mean, var);
 }
 
 // Packed-pair forms: two rows per 64-bit register pair, field parameters
@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) lwpr_kernel(LwprArgs a) {
         mean = __fadd_rn(gx, mp);
         if (VAR) var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(sm2, slv), dn), __fmul_rn(mp, mp)), 0.0f);
       } else {
-        lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, xt[r], qr, gx, &mean, &var);
+        const float2 mv = lwpr_row_exact<LAY>(a.params + h.offset, h.num_fields, xt[r], qr, gx);
+        mean = mv.x;
+        var = mv.y;
       }
       const int64_t o = row * a.row_stride + (ax - a.a_begin) * a.axis_stride;
       a.mean_out[o] = mean;

@@ -225,6 +225,13 @@ template <bool VAR, bool SECOND = false>
 __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *yy, const float *slv, float2 &den,
                                            float2 &num, float2 &m2, float2 &lv) {
   constexpr int POLY = SECOND ? (VAR ? PI2_TC_POLY_VAR_B : PI2_TC_POLY_MEAN_B) : (VAR ? PI2_TC_POLY_VAR : PI2_TC_POLY_MEAN);
+  // the batch's 8 local variances in two 128-bit loads (slv is 16-byte aligned)
+  float lvv[8];
+  if (VAR) {
+    const float4 l0 = reinterpret_cast<const float4 *>(slv)[0], l1 = reinterpret_cast<const float4 *>(slv)[1];
+    lvv[0] = l0.x; lvv[1] = l0.y; lvv[2] = l0.z; lvv[3] = l0.w;
+    lvv[4] = l1.x; lvv[5] = l1.y; lvv[6] = l1.z; lvv[7] = l1.w;
+  }
 #pragma unroll
   for (int i = 0; i < 8; i += 2) {
     const float2 x = make_float2(__uint_as_float(lg[i]), __uint_as_float(lg[i + 1]));
@@ -233,7 +240,7 @@ __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *y
     den = __fadd2_rn(den, e);
     if (VAR) {  // second moment and local variances in one sum: e (y'^2 + var_l)
       num = __ffma2_rn(e, y, num);
-      m2 = __ffma2_rn(e, __ffma2_rn(y, y, *reinterpret_cast<const float2 *>(slv + i)), m2);
+      m2 = __ffma2_rn(e, __ffma2_rn(y, y, make_float2(lvv[i], lvv[i + 1])), m2);
     } else {
       num = __ffma2_rn(e, y, num);
     }
@@ -276,7 +283,9 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
     mean = __fadd_rn(gx, mp);
     if (VAR) var = fmaxf(__fsub_rn(__fmul_rn(__fadd_rn(m2, lv), rd), __fmul_rn(mp, mp)), 0.0f);
   } else {
-    lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx, &mean, &var);
+    const float2 mv = lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, q, gx);
+    mean = mv.x;
+    var = mv.y;
   }
   a.mean_out[ax * a.plane + row] = mean;  // a warp writes 128 contiguous bytes
   if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
@@ -294,15 +303,16 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
 // on the critical path: CTAs that become resident only when the attitude kernel's
 // blocks leave the SM run it after the attitude kernel.  With many tiles the loop is
 // amortised, and that instantiation keeps its own (faster) register allocation.
-template <bool VAR, bool STREAM, bool WBULK = false>
-__global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprTcArgs a) {
-  extern __shared__ __align__(128) uint8_t tsm[];
-  __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ __align__(8) uint64_t wbar[2];  // STREAM: W slot s holds its chunk
+//
+// AX: the axis this CTA evaluates as a compile-time constant (the kernel dispatches
+// blockIdx.x % 3 to three copies of the body), so the axis' header constants are
+// immediate parameter-space operands rather than indexed constant loads; -1 = runtime.
+template <bool VAR, bool STREAM, bool WBULK, int AX>
+__device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, uint32_t &tmem_base, uint64_t &mbar,
+                                             uint64_t *wbar) {
   // CTA i evaluates axis i % 3 for tiles i / 3, i / 3 + gridDim.x / 3, ...: only that
   // axis' weights (W chunks, then its chunk-padded variances) live in shared memory
-  const int ax = blockIdx.x % 3;
+  const int ax = AX >= 0 ? AX : (int)(blockIdx.x % 3);
   const int nch = a.nchunks[ax];
   const int64_t wbeg = a.axis_off[ax], wend = ax < 2 ? a.axis_off[ax + 1] : a.w_floats;
   const int64_t nlv = (int64_t)nch * kTcChunk;
@@ -521,6 +531,26 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(LwprT
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols));
+}
+
+#ifndef PI2_TC_AXT
+#define PI2_TC_AXT 0  // 1: three axis-specialised copies of the body (harness: within 1 %, 3x code; micro/lwpr_tc_axt_b200.txt)
+#endif
+template <bool VAR, bool STREAM, bool WBULK = false>
+__global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const __grid_constant__ LwprTcArgs a) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t wbar[2];  // STREAM: W slot s holds its chunk
+#if PI2_TC_AXT
+  switch (blockIdx.x % 3) {
+    case 0: lwpr_tc_body<VAR, STREAM, WBULK, 0>(a, tsm, tmem_base, mbar, wbar); break;
+    case 1: lwpr_tc_body<VAR, STREAM, WBULK, 1>(a, tsm, tmem_base, mbar, wbar); break;
+    default: lwpr_tc_body<VAR, STREAM, WBULK, 2>(a, tsm, tmem_base, mbar, wbar); break;
+  }
+#else
+  lwpr_tc_body<VAR, STREAM, WBULK, -1>(a, tsm, tmem_base, mbar, wbar);
+#endif
 }
 
 // ---- host: W operands of the tensor-core path ------------------------------
