@@ -89,6 +89,13 @@ typedef struct pi2_cost {
   float arena_hi[3];
   float obstacles[2 * PI2_MAX_OBSTACLES]; /* (x, y) pairs */
   float threshold; /* PI2_COST_THRESHOLD: stage cost = (z > threshold) */
+  /* Opt-in uncertainty penalty kappa >= 0 (an EXTENSION: the reference's cost
+   * has no variance term, simworld.py:166-198; parity unpinned,
+   * default 0 = the reference).  With kappa > 0 and the hybrid LWPR model the
+   * sub-rollout-mean stage cost of rollout k at step t gains
+   * kappa * (sd_x^2 + sd_y^2 + sd_z^2), float32, from the LWPR predictive
+   * standard deviations of that rollout-step (dynamics.py:274-275). */
+  float variance_penalty;
 } pi2_cost;
 
 /* PiConfig fields consumed by optimize (controller.py:72-100, 374-395). */

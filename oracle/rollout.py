@@ -63,6 +63,9 @@ class Cost:
     z_floor: float = 0.05
     lo: np.ndarray = field(default_factory=lambda: np.array([-2.0, -2.0, 0.0]))
     hi: np.ndarray = field(default_factory=lambda: np.array([2.0, 2.0, 2.5]))
+    # opt-in uncertainty penalty (the engine's extension, pi2_cost.variance_penalty;
+    # NOT in the reference: 0 reproduces simworld.py:166-198)
+    variance_penalty: float = 0.0
 
     def __post_init__(self):
         self.waypoint = np.asarray(self.waypoint, float).astype(np.float32)
@@ -147,7 +150,8 @@ def run_chunk(model: Model, state, plan, lo, hi, eps, dyn_c, cost: Cost, use_spr
     xin = np.empty((ch * n, 4), np.float32)                              # :272-275
     xin.reshape(ch, n, 4)[:, :, :3] = angs[:, :n]
     xin.reshape(ch, n, 4)[:, :, 3] = u[:, :, 3]
-    mean, std = model.eval(xin, use_spread)                              # :277-279
+    pen = cost.variance_penalty > 0 and model.probabilistic              # extension (see Cost)
+    mean, std = model.eval(xin, use_spread or pen)                       # :277-279
     m_sub = dyn_c.shape[1] if use_spread else 1
     shape = (ch, m_sub, n, 3)
     acc = np.empty(shape, np.float32)
@@ -180,7 +184,12 @@ def run_chunk(model: Model, state, plan, lo, hi, eps, dyn_c, cost: Cost, use_spr
             qm = 0.5 * (qm[:, 0::2] + qm[:, 1::2])
         else:
             qm = qm.mean(axis=1, keepdims=True)
-    stage = qm[:, 0, :].astype(np.float64)                               # :320
+    qm = qm[:, 0, :]
+    if pen:  # kappa * (sd_x^2 + sd_y^2 + sd_z^2) on the sub-rollout-mean stage cost, float32
+        s3 = std.reshape(ch, n, 3)
+        tr = (s3[..., 0] * s3[..., 0] + s3[..., 1] * s3[..., 1]) + s3[..., 2] * s3[..., 2]
+        qm = qm + np.float32(cost.variance_penalty) * tr
+    stage = qm.astype(np.float64)                                        # :320
     stage *= p.dt                                                        # :321
     return np.cumsum(stage[:, ::-1], axis=1)[:, ::-1], crash             # :322
 

@@ -38,7 +38,8 @@ class Dynamics(C.Structure):
 class Cost(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_obstacles", C.c_int32), ("waypoint", C.c_float * 3),
                 ("z_floor", C.c_float), ("arena_lo", C.c_float * 3), ("arena_hi", C.c_float * 3),
-                ("obstacles", C.c_float * (2 * MAX_OBSTACLES)), ("threshold", C.c_float)]
+                ("obstacles", C.c_float * (2 * MAX_OBSTACLES)), ("threshold", C.c_float),
+                ("variance_penalty", C.c_float)]
 
 
 class OptimizeArgs(C.Structure):

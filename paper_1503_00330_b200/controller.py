@@ -311,7 +311,8 @@ def _cost_key(cost_model):
         return None
     f32 = np.float32
     return ("nav", np.asarray(wp, f32).tobytes(), np.asarray(obs, f32).tobytes(), float(f32(zf)),
-            np.asarray(lo, f32).tobytes(), np.asarray(hi, f32).tobytes())
+            np.asarray(lo, f32).tobytes(), np.asarray(hi, f32).tobytes(),
+            float(f32(getattr(cost_model, "variance_penalty", 0.0))))
 
 
 def optimize_args(cfg: PiConfig, cycle_index: int, use_graph: bool = True) -> "_abi.OptimizeArgs":

@@ -506,6 +506,7 @@ struct RollArgs {
   int model;        // PI2_MODEL_*
   int spread;       // model.probabilistic && M > 1
   int device_dyn;   // dynamics draws from the device stream (else dyn)
+  int penalty;      // cost.variance_penalty > 0 with the hybrid model: std planes are read for it
   float two_point;  // TwoPointModel magnitude
   DynParams dp;
   const float4 *xin, *ang_last;
@@ -515,6 +516,13 @@ struct RollArgs {
   double *costs;     // (K, N)
   uint8_t *crash;    // (K)
 };
+
+// opt-in uncertainty penalty (pi2_cost.variance_penalty, an extension; 0 = the
+// reference): kappa * (sd_x^2 + sd_y^2 + sd_z^2), added to the sub-rollout-mean stage
+// cost in float32
+__device__ __forceinline__ float variance_term(float kappa, float3 sd) {
+  return __fmul_rn(kappa, __fadd_rn(__fadd_rn(__fmul_rn(sd.x, sd.x), __fmul_rn(sd.y, sd.y)), __fmul_rn(sd.z, sd.z)));
+}
 
 // the LWPR kernel's output: coherent loads (see pdl_wait)
 __device__ __forceinline__ float3 ld_planes(const float *p, int64_t plane, int64_t row) {
@@ -610,7 +618,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   // the rows of step t + 1 are loaded while step t computes (hides HBM latency);
   // the analytic model's input row of step t + 1 is this step's post-step attitude row
   const bool hybrid = model == PI2_MODEL_HYBRID_LWPR;
-  const bool with_std = hybrid && a.spread;
+  const bool with_std = hybrid && (a.spread || a.penalty);
   float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
   if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, k);
   if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, k);
@@ -646,6 +654,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       mn[0] = mn[1] = mn[2] = 0.0f;
       sd[2] = a.two_point;
     }
+    const float pen = (hybrid && a.penalty) ? variance_term(cost.variance_penalty, s4) : 0.0f;
     float angterm = __fmul_rn(
         __fadd_rn(__fadd_rn(__fmul_rn(ap.x, ap.x), __fmul_rn(ap.y, ap.y)), __fmul_rn(ap.z, ap.z)), 0.2f);
     // consume the finite pad lane so ptxas keeps the in-flight prefetch registers (see
@@ -710,7 +719,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
         n = 1;
       }
     }
-    sq[t * blockDim.x + threadIdx.x] = q[0];
+    sq[t * blockDim.x + threadIdx.x] = (hybrid && a.penalty) ? __fadd_rn(q[0], pen) : q[0];
   }
 
   bool crash = false;
@@ -820,6 +829,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
     float q[SPL];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) q[j] = 0.0f;
+    const float pen = (hybrid && a.penalty) ? variance_term(cost.variance_penalty, s4) : 0.0f;
     if (active) {
       float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
       if (hybrid) {
@@ -907,6 +917,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       }
       __syncwarp();
     }
+    if (hybrid && a.penalty) qm = __fadd_rn(qm, pen);
     if (lane_g == 0) sq[t * RPB + grp] = qm;
   }
   // persistent crash of any sub-rollout (controller.py:310)
@@ -1071,9 +1082,12 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
     const unsigned b = __ballot_sync(0xffffffffu, now);
     const bool crashed = carry || (b & (0xffffffffu >> (31 - lane))) != 0;
     carry = carry || b != 0;
-    if (t < N)
+    if (t < N) {
       q[t] = threshold_cost ? (pos[2] > cost.threshold ? 1.0f : 0.0f)
                             : nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
+      if (model == PI2_MODEL_HYBRID_LWPR && a.penalty)
+        q[t] = __fadd_rn(q[t], variance_term(cost.variance_penalty, ld_planes(a.lw_std, a.lw_plane, (int64_t)t * a.K + k)));
+    }
   }
   __syncwarp();
   if (lane != 0) return;

@@ -333,6 +333,11 @@ bool spread(const pi2_ctx *ctx) {
   return prob && ctx->M > 1;
 }
 
+// the opt-in uncertainty penalty (hybrid model, navigation cost): needs the LWPR std planes
+bool penalty(const pi2_ctx *ctx) {
+  return ctx->model == PI2_MODEL_HYBRID_LWPR && ctx->cost.kind == PI2_COST_NAVIGATION && ctx->cost.variance_penalty > 0;
+}
+
 template <int MM, bool FAST>
 int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   auto *fn = rollout_kernel<MM, FAST>;
@@ -397,6 +402,8 @@ int check_ready(pi2_ctx *ctx) {
   if (!ctx->have_dyn) return fail(ctx, PI2_ERR_STATE, "dynamics not set (pi2_set_dynamics)");
   if (!ctx->have_cost) return fail(ctx, PI2_ERR_STATE, "cost plugin not set (pi2_set_cost)");
   if (ctx->model == PI2_MODEL_NONE) return fail(ctx, PI2_ERR_STATE, "model plugin not selected");
+  if (ctx->cost.kind == PI2_COST_NAVIGATION && ctx->cost.variance_penalty > 0 && ctx->model != PI2_MODEL_HYBRID_LWPR)
+    return fail(ctx, PI2_ERR_UNSUPPORTED, "variance_penalty needs a probabilistic (hybrid LWPR) model");
   return PI2_OK;
 }
 
@@ -470,11 +477,11 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   }
   CU(cudaGetLastError());
   if (ev) CU(cudaEventRecord(ev[1], st));
-  const bool sp = spread(ctx);
+  const bool sp = spread(ctx), pen = penalty(ctx);
   // LWPR outputs as planes: mean x|y|z then std x|y|z, K*N floats each
   float *lw_mean = reinterpret_cast<float *>(ctx->d_lw), *lw_std = lw_mean + 3 * K * N;
   if (ctx->model == PI2_MODEL_HYBRID_LWPR)
-    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, lw_mean, sp ? lw_std : nullptr, 1, K * N, 1, st, true));
+    TRY(launch_lwpr(ctx, 0, 3, K * N, ctx->d_xin, lw_mean, (sp || pen) ? lw_std : nullptr, 1, K * N, 1, st, true));
   if (ev) CU(cudaEventRecord(ev[2], st));
   RollArgs a{};
   a.sa = ctx->d_args;
@@ -486,6 +493,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   a.model = ctx->model;
   a.spread = sp;
   a.device_dyn = (sp && dyn_dev == nullptr) ? 1 : 0;
+  a.penalty = pen ? 1 : 0;
   a.two_point = (float)ctx->model_param;
   a.dp = ctx->dp;
   a.xin = ctx->d_xin;
@@ -773,7 +781,11 @@ int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *c) {
     return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown cost kind %d", c->kind);
   if (c->n_obstacles < 0 || c->n_obstacles > PI2_MAX_OBSTACLES)
     return fail(ctx, PI2_ERR_UNSUPPORTED, "at most %d obstacles", PI2_MAX_OBSTACLES);
-  if (ctx->have_cost && ctx->cost.kind != c->kind) invalidate_graph(ctx);  // kernel variant depends on it
+  if (!(c->variance_penalty >= 0.0f) || !std::isfinite(c->variance_penalty))
+    return fail(ctx, PI2_ERR_INVALID, "variance_penalty must be finite and >= 0");
+  // kernel variants depend on the kind and on whether the penalty is on
+  if (ctx->have_cost && (ctx->cost.kind != c->kind || (ctx->cost.variance_penalty > 0) != (c->variance_penalty > 0)))
+    invalidate_graph(ctx);
   ctx->cost = *c;
   ctx->have_cost = true;
   return PI2_OK;

@@ -35,7 +35,7 @@ def test_struct_layouts_match_header():
 
     assert C.sizeof(_abi.Dims) == 32
     assert C.sizeof(_abi.Dynamics) == 96
-    assert C.sizeof(_abi.Cost) == 4 * (2 + 3 + 1 + 3 + 3 + 32 + 1)
+    assert C.sizeof(_abi.Cost) == 4 * (2 + 3 + 1 + 3 + 3 + 32 + 1 + 1)
     assert C.sizeof(_abi.OptimizeArgs) == 8 * 8 + 8
 
 

@@ -778,3 +778,60 @@ def test_hybrid_make_batch_eval_protocol():
     mean2 = np.empty((64, 3), np.float32)
     ev(X, mean2)  # mean-only kernel variant: the same to an ulp
     np.testing.assert_allclose(mean2, mean, rtol=1e-6, atol=1e-7)
+
+
+# ---------------------------------------------------------------- opt-in uncertainty penalty
+@pytest.mark.parametrize("K,M", [(3000, 1), (20000, 1), (3000, 4), (17000, 2)])
+def test_variance_penalty_matches_oracle(K, M):
+    """The opt-in uncertainty penalty (RolloutCost(..., variance_penalty=kappa), an
+    extension of the reference's cost with parity unpinned against the reference):
+    every rollout kernel (warp per rollout K <= 8192, thread per rollout, lanes per
+    sub-rollout) against the oracle carrying the same term; kappa = 0 is the
+    reference's cost bitwise; the fused device step equals evaluate + update."""
+    N, L, kappa = 30, 48, 0.5
+    stacks = synthetic.hybrid_stacks(L, seed=K + M + 1)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=6)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn + np.array([0.02, -0.04, 0.05]))
+    plan = P.ControlPlan.hover(params, N)
+    noise = P.sample_noise(cfg, 1, 0)
+    dyn = P.sample_dynamics_noise(cfg, 1, 0) if M > 1 else None
+    eng = P.RolloutEngine(model, cfg, device=0)
+    plain = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn)
+    zero = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1, variance_penalty=0.0), dyn)
+    np.testing.assert_array_equal(zero.costs_to_go, plain.costs_to_go)
+    b = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1, variance_penalty=kappa), dyn)
+    assert np.all(b.costs_to_go[:, 0] > plain.costs_to_go[:, 0])  # the term is positive
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise,
+                         RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES, variance_penalty=kappa), dyn, M)
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL
+    dev = P.RolloutEngine(model, cfg, device=0, noise="device")
+    pcost = P.RolloutCost(task, 1, variance_penalty=kappa)
+    fused = dev.optimize_device(state, plan, pcost, cycle_index=4)
+    ctx = dev.context(K, N)
+    eps = np.empty((K, N, 4))
+    ctx.call("pi2_device_noise", _abi.STREAM_CONTROL, cfg.rng_seed, 4, 0, _abi.ptr(cfg.exploration_std), _abi.ptr(eps))
+    dn = None
+    if M > 1:
+        dn = np.empty((K, M, N, 3), np.float32)
+        ctx.call("pi2_device_noise", _abi.STREAM_DYNAMICS, cfg.rng_seed, 4, 0, None, _abi.ptr(dn))
+    bb = eng.evaluate(state, plan, eps, pcost, dn)
+    np.testing.assert_array_equal(fused.controls, P.path_integral_update(plan, bb, cfg.temperature).controls)
+    # switching the penalty off again re-captures the step: back to the reference's cost
+    off = dev.optimize_device(state, plan, P.RolloutCost(task, 1), cycle_index=4)
+    bb0 = eng.evaluate(state, plan, eps, P.RolloutCost(task, 1), dn)
+    np.testing.assert_array_equal(off.controls, P.path_integral_update(plan, bb0, cfg.temperature).controls)
+
+
+def test_variance_penalty_needs_probabilistic_model():
+    p = P.QuadParams()
+    cfg = P.PiConfig(num_rollouts=64, horizon_steps=10, iterations_per_step=1)
+    eng = P.RolloutEngine(P.AnalyticModel(p), cfg, device=0)
+    with pytest.raises(TypeError, match="variance_penalty"):
+        eng.evaluate(P.QuadState.hover((0, 0, 1)), P.ControlPlan.hover(p, 10), np.zeros((64, 10, 4)),
+                     P.RolloutCost(P.Task.default(), 0, variance_penalty=1.0))
