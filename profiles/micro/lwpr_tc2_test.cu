@@ -1,0 +1,173 @@
+// Tensor-core LWPR (lwpr_tc_kernel) vs the CUDA-core kernel on a C2-sized batch:
+// max |diff| of mean/std and device time of both.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//          -I paper_1503_00330_b200/csrc -o lwpr_tc_test profiles/micro/lwpr_tc_test.cu
+#include <cstdio>
+#include <algorithm>
+#include <vector>
+
+#include "lwpr_tc2.cuh"  // profiles/micro/lwpr_tc2.cuh (record); build with -I profiles/micro -DPI2_TC_CHUNK=32
+
+using namespace pi2;
+
+static uint64_t s_rng = 88172645463325252ull;
+static double urand() {
+  s_rng ^= s_rng << 13; s_rng ^= s_rng >> 7; s_rng ^= s_rng << 17;
+  return (s_rng >> 11) * (1.0 / 9007199254740992.0);
+}
+
+int main(int argc, char **argv) {
+  const int64_t rows = argc > 1 ? atoll(argv[1]) : 65536ll * 50;
+  const int L = argc > 2 ? atoi(argv[2]) : 100;
+  AxisRaw ax[3];
+  const double lo[4] = {-0.35, -0.35, -0.35, 0.10}, hi[4] = {0.35, 0.35, 0.35, 0.28};
+  const double md[4] = {30, 30, 30, 1500};
+  for (auto &a : ax) {
+    a.L = L; a.d = 4;
+    for (int l = 0; l < L; ++l) {
+      for (int i = 0; i < 4; ++i) a.centers.push_back(lo[i] + (hi[i] - lo[i]) * urand());
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) a.metrics.push_back(i == j ? md[i] : 0.0);
+      for (int i = 0; i < 5; ++i) a.coefs.push_back(4.0 * (urand() - 0.5));
+      a.lvar.push_back(0.01 + 0.09 * urand());
+    }
+  }
+  std::vector<float> rec;
+  AxisHeader hdr[3];
+  for (int i = 0; i < 3; ++i) fold_axis(ax[i], kLayShared, rec, hdr[i]);
+  std::vector<float> blob;
+  LwprTcArgs ta{};
+  if (!build_tc_weights(ax, blob, ta)) { printf("not tc-eligible\n"); return 1; }
+  std::vector<float4> hx(rows);
+  for (auto &v : hx)
+    v = make_float4(0.8 * (urand() - 0.5), 0.8 * (urand() - 0.5), 0.8 * (urand() - 0.5), 0.05 + 0.3 * urand());
+  float4 *dx; float *dparams, *dblob, *m1, *s1, *m2, *s2;
+  cudaMalloc(&dx, rows * 16); cudaMalloc(&m1, rows * 16); cudaMalloc(&s1, rows * 16);
+  cudaMalloc(&m2, rows * 16); cudaMalloc(&s2, rows * 16);
+  cudaMalloc(&dparams, rec.size() * 4); cudaMalloc(&dblob, blob.size() * 4);
+  cudaMemcpy(dx, hx.data(), rows * 16, cudaMemcpyHostToDevice);
+  cudaMemcpy(dparams, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dblob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice);
+
+  LwprArgs la{};
+  la.params = dparams;
+  for (int i = 0; i < 3; ++i) la.axis[i] = hdr[i];
+  la.a_begin = 0; la.a_end = 3; la.layout = kLayShared; la.resident = 1;
+  la.rows = rows; la.x = dx; la.mean_out = m1; la.sd_out = s1; la.row_stride = 1; la.axis_stride = rows; la.sqrt_out = 1;
+  const int smem1 = (int)(rec.size() * 4);
+  auto *k1 = lwpr_kernel<kLayShared, true, 8>;
+  cudaFuncSetAttribute((const void *)k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+  const unsigned g1 = (unsigned)((rows + 1023) / 1024);
+
+  ta.params = dparams;
+  for (int i = 0; i < 3; ++i) ta.axis[i] = hdr[i];
+  ta.w = dblob; ta.rows = rows; ta.x = dx; ta.mean_out = m2; ta.sd_out = s2; ta.plane = rows; ta.sqrt_out = 1;
+  int64_t wmax = 0;
+  for (int i = 0; i < 3; ++i) {
+    const int64_t we = i < 2 ? ta.axis_off[i + 1] : ta.w_floats;
+    wmax = std::max<int64_t>(wmax, we - ta.axis_off[i] + (int64_t)ta.nchunks[i] * kTcChunk);
+  }
+  // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
+  int64_t lvmax = 0;
+  for (int i = 0; i < 3; ++i) lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
+  auto *k2 = lwpr_tc_kernel<true, false>;
+  auto *k4 = lwpr_tc_kernel<false, false>;
+  int smem2 = tc_smem_bytes(wmax, (const void *)k2);
+  const bool stream = smem2 < 0 || getenv("STREAM");
+  if (stream) {  // W streamed per chunk
+    k2 = lwpr_tc_kernel<true, true>;
+    k4 = lwpr_tc_kernel<false, true>;
+    smem2 = tc_smem_bytes(2 * kTcWSlotFloats + lvmax, (const void *)k2);
+  }
+  printf("W %s\n", stream ? "streamed" : "resident");
+  if (smem2 < 0) { printf("does not fit %d CTAs/SM\n", kTcCtasPerSm); return 1; }
+  cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned g2 = (kTcCtasPerSm * sms) / 3 * 3;
+  printf("CTAS %d CHUNK %d\n", PI2_TC_CTAS, PI2_TC_CHUNK);
+  printf("rows %lld L %d: W %lld floats, lv %lld, smem tc %d B, chunks %d pad %d\n", (long long)rows, L,
+         (long long)ta.w_floats, (long long)ta.lv_floats, smem2, ta.nchunks[0], ta.chunk_pad[0][0]);
+
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float ms1, ms2;
+  k1<<<g1, 128, smem1>>>(la);
+  k2<<<g2, kTcThreads, smem2>>>(ta);
+  cudaError_t err = cudaDeviceSynchronize();
+  printf("first run: %s\n", cudaGetErrorString(err));
+  if (err != cudaSuccess) return 2;
+  cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k1<<<g1, 128, smem1>>>(la); cudaEventRecord(e1);
+  cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
+  cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k2<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
+  cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+  {  // chunk-pipelined kernel (lwpr_tc2_kernel): same numerics, must match bitwise
+    auto *k5 = lwpr_tc2_kernel<true>;
+    auto *k6 = lwpr_tc2_kernel<false>;
+    cudaFuncSetAttribute((const void *)k5, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute((const void *)k6, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    float *m3, *s3;
+    cudaMalloc(&m3, rows * 16); cudaMalloc(&s3, rows * 16);
+    LwprTcArgs tb = ta; tb.mean_out = m3; tb.sd_out = s3;
+    k5<<<g2, kTcThreads, smem2>>>(tb);
+    printf("tc2 first run: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    float ms5, ms6;
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k5<<<g2, kTcThreads, smem2>>>(tb); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms5, e0, e1);
+    std::vector<float> x1(rows * 3), x2(rows * 3), y1(rows * 3), y2(rows * 3);
+    cudaMemcpy(x1.data(), m2, rows * 12, cudaMemcpyDeviceToHost); cudaMemcpy(x2.data(), m3, rows * 12, cudaMemcpyDeviceToHost);
+    cudaMemcpy(y1.data(), s2, rows * 12, cudaMemcpyDeviceToHost); cudaMemcpy(y2.data(), s3, rows * 12, cudaMemcpyDeviceToHost);
+    int64_t diff = 0;
+    for (int64_t i = 0; i < rows * 3; ++i) diff += (memcmp(&x1[i], &x2[i], 4) != 0) + (memcmp(&y1[i], &y2[i], 4) != 0);
+    tb.sd_out = nullptr;
+    k6<<<g2, kTcThreads, smem2>>>(tb);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k6<<<g2, kTcThreads, smem2>>>(tb); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms6, e0, e1);
+    printf("tc2: variance %8.1f us  mean-only %8.1f us  bitwise differences vs tc %lld  (%s)\n", ms5 / 5 * 1e3,
+           ms6 / 5 * 1e3, (long long)diff, cudaGetErrorString(cudaDeviceSynchronize()));
+  }
+#ifdef PI2_TC_PROF
+  {
+    unsigned long long pr[5];
+    cudaMemcpyFromSymbol(pr, g_tc_prof, sizeof(pr));
+    double tot = 0;
+    for (auto v : pr) tot += (double)v;
+    const double n = 6.0 * ((rows + 127) / 128) * 3 * 4;  // warp-tile-axes over 6 launches (4 row warps per CTA)
+    printf("clocks per warp-tile-axis: features+finalize %.0f  barrier %.0f  mma-wait %.0f  exp %.0f  tail %.0f  total %.0f\n",
+           pr[0] / n, pr[1] / n, pr[2] / n, pr[3] / n, pr[4] / n, tot / n);
+  }
+#endif
+  std::vector<float> a1(rows * 4), b1(rows * 4), a2(rows * 4), b2(rows * 4);
+  cudaMemcpy(a1.data(), m1, rows * 16, cudaMemcpyDeviceToHost); cudaMemcpy(b1.data(), s1, rows * 16, cudaMemcpyDeviceToHost);
+  cudaMemcpy(a2.data(), m2, rows * 16, cudaMemcpyDeviceToHost); cudaMemcpy(b2.data(), s2, rows * 16, cudaMemcpyDeviceToHost);
+  double dm = 0, ds = 0, mm = 0;
+  int64_t bad = 0;
+  for (int64_t i = 0; i < rows * 4; ++i) {
+    const double d1 = fabs(a1[i] - a2[i]), d2 = fabs(b1[i] - b2[i]) / fmax(1e-6, fabs(b1[i]));
+    if (!(d1 <= 1e30)) ++bad;
+    dm = fmax(dm, d1); ds = fmax(ds, d2); mm = fmax(mm, fabs(a1[i]));
+  }
+  const double flops = (double)rows * 3 * L * 32;
+  printf("cuda-core: %8.1f us (%.1f TFLOP/s alg)   tensor-core: %8.1f us (%.1f TFLOP/s alg)\n", ms1 / 5 * 1e3,
+         flops / (ms1 / 5) / 1e9, ms2 / 5 * 1e3, flops / (ms2 / 5) / 1e9);
+  printf("max |dmean| %.3e (max |mean| %.2f), max rel dstd %.3e, nan/inf %lld\n", dm, mm, ds, (long long)bad);
+  printf("sample: cc %f %f tc %f %f\n", a1[0], b1[0], a2[0], b2[0]);
+  {  // mean only (M = 1 rollouts)
+    auto *k3 = lwpr_kernel<kLayShared, false, 8>;
+    cudaFuncSetAttribute((const void *)k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+    cudaFuncSetAttribute((const void *)k4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    la.sd_out = nullptr;
+    ta.sd_out = nullptr;
+    k3<<<g1, 128, smem1>>>(la);
+    k4<<<g2, kTcThreads, smem2>>>(ta);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k3<<<g1, 128, smem1>>>(la); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k4<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+    cudaMemcpy(a1.data(), m1, rows * 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(a2.data(), m2, rows * 16, cudaMemcpyDeviceToHost);
+    double dm0 = 0;
+    for (int64_t i = 0; i < rows * 4; ++i) dm0 = fmax(dm0, fabs(a1[i] - a2[i]));
+    printf("mean-only  cuda-core: %8.1f us   tensor-core: %8.1f us   max |dmean| %.3e   (%s)\n", ms1 / 5 * 1e3,
+           ms2 / 5 * 1e3, dm0, cudaGetErrorString(cudaDeviceSynchronize()));
+  }
+  return 0;
+}
