@@ -128,6 +128,18 @@ __global__ void __launch_bounds__(kRolloutBlock)
   const Key128 ck = DEVICE_NOISE ? iter_key(sa->key_prefix[0], (uint64_t)iteration) : Key128{0, 0};
   float4 *xk = xin + k;  // row (k, t) at xk[t * K]
   constexpr int TB = PI2_ATT_TB;  // noise of TB steps is generated before their serial FP64 recurrence
+  // host noise (the reference's streams in HBM): the next TB steps' rows are loaded while
+  // this block's recurrence runs, so the DRAM latency is not exposed once per block
+  double2 en[TB][2];
+  auto load_block = [&](int t0) {
+#pragma unroll
+    for (int j = 0; j < TB; ++j) {
+      const int t = t0 + j < N ? t0 + j : N - 1;
+      en[j][0] = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
+      en[j][1] = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
+    }
+  };
+  if (!DEVICE_NOISE) load_block(0);
 #pragma unroll(kAttUnroll)
   for (int t0 = 0; t0 < N; t0 += TB) {
     double e[TB][4];
@@ -139,11 +151,10 @@ __global__ void __launch_bounds__(kRolloutBlock)
         if (zout && t0 + j < N) zout[(int64_t)t * K + k] = z;
         eps_from_z(sa, z, e[j]);
       } else {
-        const double2 a = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t));
-        const double2 b = __ldg(reinterpret_cast<const double2 *>(ek + 4 * t) + 1);
-        e[j][0] = a.x; e[j][1] = a.y; e[j][2] = b.x; e[j][3] = b.y;
+        e[j][0] = en[j][0].x; e[j][1] = en[j][0].y; e[j][2] = en[j][1].x; e[j][3] = en[j][1].y;
       }
     }
+    if (!DEVICE_NOISE && t0 + TB < N) load_block(t0 + TB);
 #pragma unroll
     for (int j = 0; j < TB; ++j) {
       const int t = t0 + j;
