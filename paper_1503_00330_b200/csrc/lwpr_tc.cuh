@@ -156,14 +156,44 @@ constexpr int kTcABytes = 8192;  // one A operand: hi | lo, 128 rows x 8 tf32 ea
 
 #ifdef PI2_TC_PROF
 __device__ unsigned long long g_tc_prof[5];  // clocks: features+finalize, barrier, MMA wait, exp, tail
+#define PI2_TC_TDECL long long prof[5] = {0, 0, 0, 0, 0}, t_last = clock64();
 #define PI2_TC_T(i)                          \
   {                                          \
     const long long t_ = clock64();          \
     prof[i] += t_ - t_last;                  \
     t_last = t_;                             \
   }
+#define PI2_TC_TFLUSH                                                                   \
+  if ((threadIdx.x & 31) == 0)                                                          \
+    for (int k_ = 0; k_ < 5; ++k_) atomicAdd(&g_tc_prof[k_], (unsigned long long)prof[k_]);
+#elif defined(PI2_TC_TRACE)
+// phase trace (experiments): lane 0 of every warp on SM 0 logs (clock, hw warp slot, CTA,
+// phase end) into its own region (one atomic per warp to claim it, then plain stores)
+constexpr int kTcTraceCap = 4096;  // events per warp
+__device__ unsigned long long g_tc_trace[64 * kTcTraceCap];
+__device__ unsigned int g_tc_trace_n;  // warps that claimed a region
+__device__ int g_tc_trace_on;
+__device__ __forceinline__ int tc_trace_claim() {
+  unsigned sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if (sm != 0 || (threadIdx.x & 31) != 0 || !g_tc_trace_on) return -1;
+  const unsigned w = atomicAdd(&g_tc_trace_n, 1u);
+  return w < 64 ? (int)w : -1;
+}
+__device__ __forceinline__ void tc_trace(int slot, int &n, int i) {
+  if (slot < 0 || n >= kTcTraceCap) return;
+  unsigned wid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  g_tc_trace[slot * kTcTraceCap + n++] =
+      ((unsigned long long)clock64() << 20) | ((blockIdx.x & 0x3ffu) << 10) | ((wid & 63u) << 4) | (unsigned)i;
+}
+#define PI2_TC_TDECL const int tr_slot_ = tc_trace_claim(); int tr_n_ = 0;
+#define PI2_TC_T(i) tc_trace(tr_slot_, tr_n_, i)
+#define PI2_TC_TFLUSH
 #else
+#define PI2_TC_TDECL
 #define PI2_TC_T(i)
+#define PI2_TC_TFLUSH
 #endif
 
 // software-pipelined TMEM loads in the exp loop (runtime batch loop): 0 never, 1 streamed
@@ -291,6 +321,82 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
   if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
 }
 
+// The exp phase of nf (multiple of 8) fields of this warp's 32 rows, read from TMEM
+// (logits from column tmem_lane, y' lc columns further on), 2^x + moments into the
+// accumulators.  nf == NFULL runs a fully unrolled loop (compile-time batch count).
+template <bool VAR, bool STREAM, int NFULL>
+__device__ __forceinline__ void tc_exp_span(uint32_t tmem_lane, int lc, int nf, const float *slv, float2 &den,
+                                            float2 &num, float2 &m2, float2 &lv) {
+  const int nb = nf >> 3;  // 8-field batches, two per TMEM wait
+  if constexpr (PI2_TC_LDPIPE == 2 || (PI2_TC_LDPIPE == 1 && STREAM)) {
+  // each batch's TMEM load is in flight while the previous batch computes
+  // (tcgen05.wait::ld waits for all of a thread's loads: load b + 1, compute b, wait)
+  uint32_t la[8], ya[8], lb[8], yb[8];
+  PI2_TMEM_LD8(la, tmem_lane);
+  PI2_TMEM_LD8(ya, tmem_lane + lc);
+  PI2_TMEM_WAIT16(la, ya);
+  for (int b = 0; b < nb; b += 2) {
+    if (b + 1 < nb) {
+      PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
+      PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+    }
+    tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
+    if (b + 1 < nb) {
+      PI2_TMEM_WAIT16(lb, yb);
+      if (b + 2 < nb) {
+        PI2_TMEM_LD8(la, tmem_lane + 8 * b + 16);
+        PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b + 16);
+      }
+      tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+      if (b + 2 < nb) PI2_TMEM_WAIT16(la, ya);
+    }
+  }
+  } else {
+  auto batches = [&](auto nb_c) {  // nb_c: compile-time batch count, or 0 = runtime nb
+    constexpr int NBC = decltype(nb_c)::value;
+    const int n = NBC > 0 ? NBC : nb;
+#if PI2_TC_LD16
+    // 16-column TMEM loads, one per operand per batch pair: variance loop only (harness L=100
+    // 411 -> 406 us, L=200 704 -> 692 us); the mean-only loop spills with them and loses 4-5 %
+    if constexpr (VAR && NBC > 0 && NBC % 2 == 0) {
+#pragma unroll
+      for (int b = 0; b < NBC; b += 2) {
+        uint32_t l16[16], y16[16];
+        PI2_TMEM_LD16(l16, tmem_lane + 8 * b);
+        PI2_TMEM_LD16(y16, tmem_lane + lc + 8 * b);
+        PI2_TMEM_WAIT16(l16, y16);
+        PI2_TMEM_WAIT16(l16 + 8, y16 + 8);
+        tc_fields8<VAR>(l16, y16, slv + 8 * b, den, num, m2, lv);
+        tc_fields8<VAR, true>(l16 + 8, y16 + 8, slv + 8 * b + 8, den, num, m2, lv);
+      }
+      return;
+    }
+#endif
+#pragma unroll
+    for (int b = 0; b < (NBC > 0 ? NBC : 1 << 30); b += 2) {
+      if (NBC == 0 && b >= n) break;
+      uint32_t la[8], ya[8], lb[8], yb[8];
+      PI2_TMEM_LD8(la, tmem_lane + 8 * b);
+      PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b);
+      if (b + 1 < n) {
+        PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
+        PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
+      }
+      PI2_TMEM_WAIT16(la, ya);
+      PI2_TMEM_WAIT16(lb, yb);
+      tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
+      if (b + 1 < n) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
+    }
+  };
+#if PI2_TC_UNROLL
+  if (nf == NFULL) batches(std::integral_constant<int, NFULL / 8>{});
+  else batches(std::integral_constant<int, 0>{});
+#else
+  batches(std::integral_constant<int, 0>{});
+#endif
+  }
+}
+
 // Per CTA the tiles are software-pipelined: while the tensor core computes the
 // first chunk of tile t, the CUDA cores finalize tile t - 1 and write tile t + 1's
 // features into the other A buffer (its x was loaded one tile ahead), so only the
@@ -393,9 +499,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
   const uint32_t sw_addr = (uint32_t)__cvta_generic_to_shared(sw);
   uint32_t phase = 0, nw = 0;  // nw: chunks issued by this CTA (W ring position)
   int buf = 0;
-#ifdef PI2_TC_PROF
-  long long prof[5] = {0, 0, 0, 0, 0}, t_last = clock64();
-#endif
+  PI2_TC_TDECL
 
   // WBULK: the resident W landed (thread 0 issues every MMA)
   if (WBULK && tid == 0 && tile < ntiles) mbar_wait(wbar_addr, 0);
@@ -439,75 +543,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;");
       PI2_TC_T(2);
-      const float *slv = slv_base + (int64_t)c * kTcChunk;
-      const int nb = lc >> 3;  // 8-field batches, two per TMEM wait
-      if constexpr (PI2_TC_LDPIPE == 2 || (PI2_TC_LDPIPE == 1 && STREAM)) {
-      // each batch's TMEM load is in flight while the previous batch computes
-      // (tcgen05.wait::ld waits for all of a thread's loads: load b + 1, compute b, wait)
-      uint32_t la[8], ya[8], lb[8], yb[8];
-      PI2_TMEM_LD8(la, tmem_lane);
-      PI2_TMEM_LD8(ya, tmem_lane + lc);
-      PI2_TMEM_WAIT16(la, ya);
-      for (int b = 0; b < nb; b += 2) {
-        if (b + 1 < nb) {
-          PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
-          PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
-        }
-        tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
-        if (b + 1 < nb) {
-          PI2_TMEM_WAIT16(lb, yb);
-          if (b + 2 < nb) {
-            PI2_TMEM_LD8(la, tmem_lane + 8 * b + 16);
-            PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b + 16);
-          }
-          tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
-          if (b + 2 < nb) PI2_TMEM_WAIT16(la, ya);
-        }
-      }
-      } else {
-      auto batches = [&](auto nb_c) {  // nb_c: compile-time batch count, or 0 = runtime nb
-        constexpr int NBC = decltype(nb_c)::value;
-        const int n = NBC > 0 ? NBC : nb;
-#if PI2_TC_LD16
-        // 16-column TMEM loads, one per operand per batch pair: variance loop only (harness L=100
-        // 411 -> 406 us, L=200 704 -> 692 us); the mean-only loop spills with them and loses 4-5 %
-        if constexpr (VAR && NBC > 0 && NBC % 2 == 0) {
-#pragma unroll
-          for (int b = 0; b < NBC; b += 2) {
-            uint32_t l16[16], y16[16];
-            PI2_TMEM_LD16(l16, tmem_lane + 8 * b);
-            PI2_TMEM_LD16(y16, tmem_lane + lc + 8 * b);
-            PI2_TMEM_WAIT16(l16, y16);
-            PI2_TMEM_WAIT16(l16 + 8, y16 + 8);
-            tc_fields8<VAR>(l16, y16, slv + 8 * b, den, num, m2, lv);
-            tc_fields8<VAR, true>(l16 + 8, y16 + 8, slv + 8 * b + 8, den, num, m2, lv);
-          }
-          return;
-        }
-#endif
-#pragma unroll
-        for (int b = 0; b < (NBC > 0 ? NBC : 1 << 30); b += 2) {
-          if (NBC == 0 && b >= n) break;
-          uint32_t la[8], ya[8], lb[8], yb[8];
-          PI2_TMEM_LD8(la, tmem_lane + 8 * b);
-          PI2_TMEM_LD8(ya, tmem_lane + lc + 8 * b);
-          if (b + 1 < n) {
-            PI2_TMEM_LD8(lb, tmem_lane + 8 * b + 8);
-            PI2_TMEM_LD8(yb, tmem_lane + lc + 8 * b + 8);
-          }
-          PI2_TMEM_WAIT16(la, ya);
-          PI2_TMEM_WAIT16(lb, yb);
-          tc_fields8<VAR>(la, ya, slv + 8 * b, den, num, m2, lv);
-          if (b + 1 < n) tc_fields8<VAR, true>(lb, yb, slv + 8 * b + 8, den, num, m2, lv);
-        }
-      };
-#if PI2_TC_UNROLL
-      if (lc == kTcChunk) batches(std::integral_constant<int, kTcChunk / 8>{});
-      else batches(std::integral_constant<int, 0>{});
-#else
-      batches(std::integral_constant<int, 0>{});
-#endif
-      }
+      tc_exp_span<VAR, STREAM, kTcChunk>(tmem_lane, lc, lc, slv_base + (int64_t)c * kTcChunk, den, num, m2, lv);
       woff += (int64_t)2 * (2 * lc * 8);
       PI2_TC_T(3);
     }
@@ -524,14 +560,13 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
   asm volatile("tcgen05.fence::before_thread_sync;");
   tc_finalize<VAR>(a, h, ax, row_prev, xt_prev, q_prev, dn_p, nm_p, m2_p, lv_p);
   PI2_TC_T(4);
-#ifdef PI2_TC_PROF
-  if ((tid & 31) == 0)
-    for (int i = 0; i < 5; ++i) atomicAdd(&g_tc_prof[i], (unsigned long long)prof[i]);
-#endif
+  PI2_TC_TFLUSH
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols));
 }
+
+
 
 #ifndef PI2_TC_AXT
 #define PI2_TC_AXT 0  // 1: three axis-specialised copies of the body (harness: within 1 %, 3x code; micro/lwpr_tc_axt_b200.txt)
@@ -551,6 +586,279 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const
 #else
   lwpr_tc_body<VAR, STREAM, WBULK, -1>(a, tsm, tmem_base, mbar, wbar);
 #endif
+}
+
+
+// ---- column-split, TMEM double-buffered schedule (lwpr_tc3_kernel) ----------
+// Phase traces of lwpr_tc_kernel (micro/tc_trace_b200.txt) show each warp in its exp
+// phase only ~36 % of the time (CTA barrier 24 %, MMA wait 22 %, features + finalize
+// 17 %): the next chunk's MMA can only start once the slowest warp has read the
+// current chunk out of the CTA's single TMEM buffer, and it takes ~450-600 clocks
+// (micro/mma_lat_b200.txt).  So only ~1.4 warps per SM sub-partition feed MUFU on
+// average, while the exp loop alone reaches 61 % of MUFU peak with one warp and 77 % with
+// four (micro/exp_loop_rate_b200.txt).  A split barrier alone does not help
+// (micro/lwpr_tc_splitbar_b200.txt): the critical path runs through the MMA.
+//
+// Here a CTA has 8 warps and 256 TMEM columns = two chunk buffers (2 CTAs per SM, the
+// same 16 warps and 512 columns per SM).  Warps w and w + 4 own the same 32 rows (TMEM
+// lanes 32 (w % 4) ..) and split every chunk's fields (w: the first half, rounded down to
+// 8, w + 4: the rest).  Item j = (tile, chunk) lives in buffer j & 1; the MMA of item
+// j + 2 is issued by thread 0 as soon as every warp has read item j (a named barrier:
+// warp 0 bar.sync, the others bar.arrive), so it runs while the warps are in item
+// j + 1's exp phase and no warp waits for an MMA unless it runs a whole item ahead.
+// The low warps also write the features (tile t's, into A[t % 3], before item
+// t * nch - 2 is released) and hand their partial moments to the high warps through
+// shared memory + an mbarrier; the high warps finalize.  Per row, den / num / m2 are the
+// sums of the two halves' sums (a different association than lwpr_tc_kernel: equal
+// within rounding).
+#ifndef PI2_TC3_SPLIT
+#define PI2_TC3_SPLIT 1
+#endif
+constexpr int kTc3Threads = 128 * PI2_TC3_SPLIT;
+constexpr int kTc3CtasPerSm = 2;
+constexpr int kTc3TmemCols = 2 * kTcTmemCols;  // two chunk buffers
+constexpr int kTc3ABuf = 3;
+constexpr int kTc3Stash = 4;  // (g(x), probe) slots: tile t in t % 4
+constexpr int kTc3ExtraBytes = kTc3ABuf * kTcABytes + kTc3Stash * 128 * 8 + 2 * 128 * 16;  // A, stash, partials
+
+template <bool VAR>
+__device__ __forceinline__ void tc_finalize3(const LwprTcArgs &a, const AxisHeader &h, int ax, int64_t row, float gx,
+                                             float fin, float dn, float nm, float m2) {
+  if (row >= a.rows) return;
+  float mean, var = 0.0f;
+  if (dn >= kSlowDen && dn <= 3.0e38f && isfinite(fin)) {
+    const float rd = rcp_fma(dn);
+    const float mp = __fmul_rn(nm, rd);
+    mean = __fadd_rn(gx, mp);
+    if (VAR) var = fmaxf(__fsub_rn(__fmul_rn(m2, rd), __fmul_rn(mp, mp)), 0.0f);
+  } else {  // rare: the centred inputs again, for the exact path
+    const float4 x = __ldcg(a.x + row);
+    const float4 xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]),
+                                  __fsub_rn(x.w, h.mu[3]));
+    const float2 mv = lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, shared_qrow(h, xt), gx);
+    mean = mv.x;
+    var = mv.y;
+  }
+  a.mean_out[ax * a.plane + row] = mean;  // a warp writes 128 contiguous bytes
+  if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// SPLIT = 2: 8 warps, each chunk's fields split between warps w and w + 4 (above).
+// SPLIT = 1: 4 warps, each reads its rows' whole chunk: an item's exp phase (64 fields)
+// outlasts the MMA of the item two ahead, which the split halves do not.
+template <bool VAR, bool STREAM, bool WBULK, int SPLIT = PI2_TC3_SPLIT>
+__global__ void __launch_bounds__(128 * SPLIT, kTc3CtasPerSm) lwpr_tc3_kernel(const __grid_constant__ LwprTcArgs a) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t full[2];    // MMA of the item in buffer b complete
+  __shared__ __align__(8) uint64_t wbar[2];    // STREAM: W slot s holds its chunk; WBULK: resident W landed
+  __shared__ __align__(8) uint64_t pready[8];  // quarter q, slot s: low warp's partial moments of a tile written
+  const int ax = (int)(blockIdx.x % 3);
+  const int nch = a.nchunks[ax];
+  const int64_t wbeg = a.axis_off[ax], wend = ax < 2 ? a.axis_off[ax + 1] : a.w_floats;
+  const int64_t nlv = (int64_t)nch * kTcChunk;
+  const int64_t wfl = STREAM ? 2 * kTcWSlotFloats : wend - wbeg;
+  float *sw = reinterpret_cast<float *>(tsm);
+  float *slv_base = sw + wfl;
+  uint8_t *sa = tsm + (((wfl + nlv) * 4 + 127) / 128) * 128;                // kTc3ABuf A operands
+  float2 *stash = reinterpret_cast<float2 *>(sa + kTc3ABuf * kTcABytes);       // (g(x), probe) per A slot and row
+  float4 *part = reinterpret_cast<float4 *>(stash + kTc3Stash * 128);         // low half's moments per slot and row
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int half = SPLIT == 2 ? warp >> 2 : 0, quarter = warp & 3;
+  const int row_in_tile = quarter * 32 + lane;
+
+  if (!STREAM && !WBULK)
+    for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
+      reinterpret_cast<float4 *>(sw)[i] = __ldg(reinterpret_cast<const float4 *>(a.w + wbeg) + i);
+  for (int64_t i = tid; i < nlv; i += blockDim.x) slv_base[i] = __ldg(a.w + a.lv_off[ax] + i);
+  const uint32_t wbar_addr = (uint32_t)__cvta_generic_to_shared(&wbar[0]);
+  const uint32_t full_addr = (uint32_t)__cvta_generic_to_shared(&full[0]);
+  const uint32_t pready_addr = (uint32_t)__cvta_generic_to_shared(&pready[0]);
+  const uint32_t sw_addr = (uint32_t)__cvta_generic_to_shared(sw);
+  auto load_w = [&](int c, uint32_t slot) {  // thread 0: chunk c's W into ring slot `slot`
+    const uint32_t bytes = (uint32_t)(2 * 2 * a.chunk_pad[ax][c] * 8 * 4);
+    const uint32_t bar = wbar_addr + 8 * slot;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            sw_addr + slot * (uint32_t)(kTcWSlotFloats * 4)),
+        "l"(a.w + wbeg + a.chunk_woff[ax][c]), "r"(bytes), "r"(bar)
+        : "memory");
+  };
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "n"(kTc3TmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const AxisHeader &h = a.axis[ax];
+  const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
+  const int64_t tstride = gridDim.x / 3, tile0 = blockIdx.x / 3;
+  const int64_t nt = tile0 < ntiles ? (ntiles - tile0 + tstride - 1) / tstride : 0;  // tiles of this CTA
+  const int64_t nitems = nt * nch;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_addr));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_addr + 8));
+    for (int i = 0; i < 8; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(pready_addr + 8 * i));
+    if (STREAM || WBULK) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr + 8));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    if (STREAM) {
+      if (nitems > 0) load_w(0, 0);
+      if (nitems > 1) load_w(1 % nch, 1);
+    } else if (WBULK && nt > 0) {
+      const uint32_t bytes = (uint32_t)((wend - wbeg) * 4);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wbar_addr), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sw_addr),
+          "l"(a.w + wbeg), "r"(bytes), "r"(wbar_addr)
+          : "memory");
+    }
+  }
+  auto row_of = [&](int64_t i) { return (tile0 + i * tstride) * 128 + row_in_tile; };
+  auto load_x = [&](int64_t i) {
+    const int64_t r = row_of(i);
+    return __ldcg(a.x + (r < last ? r : last));
+  };
+  // low warps: tile i's features -> A[i % 3], its g(x) and finiteness probe -> stash
+  auto features = [&](int64_t i, float4 x) {
+    float4 xt;
+    float q;
+    tc_features(h, x, sa + (int)(i % kTc3ABuf) * kTcABytes, row_in_tile, xt, q);
+    const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
+    stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile] =
+        make_float2(gx, __fadd_rn(__fadd_rn(xt.x, xt.y), __fadd_rn(__fadd_rn(xt.z, xt.w), q)));
+  };
+  // x comes from the attitude kernel: wait for it, then coherent loads (see lwpr_tc_body)
+  pdl_wait();
+  int64_t fnext = 0;  // next tile whose features the low warps write
+  float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (half == 0) {
+    const int64_t pro = nch == 1 ? 2 : 1;  // tiles staged before the first MMA  // tiles staged before the first MMA
+    for (; fnext < pro && fnext < nt; ++fnext) features(fnext, load_x(fnext));
+    if (fnext < nt) xn = load_x(fnext);
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  const uint32_t tmem_lane = tmem + ((uint32_t)(quarter * 32) << 16);
+  const uint32_t sa_addr0 = (uint32_t)__cvta_generic_to_shared(sa);
+  // thread 0: the 3 MMAs of item j = (tile i, chunk c) into buffer j & 1
+  auto issue = [&](int64_t i, int c, int64_t j) {
+    const int lc = a.chunk_pad[ax][c];
+    const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
+    const uint32_t sa_addr = sa_addr0 + (uint32_t)(i % kTc3ABuf) * kTcABytes;
+    const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
+    if (STREAM) mbar_wait(wbar_addr + 8 * (uint32_t)(j & 1), (uint32_t)((j >> 1) & 1));  // its W landed
+    const uint32_t wb = STREAM ? sw_addr + (uint32_t)(j & 1) * (uint32_t)(kTcWSlotFloats * 4)
+                               : sw_addr + (uint32_t)(a.chunk_woff[ax][c] * 4);
+    const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
+    const uint32_t d = tmem + (uint32_t)(j & 1) * (uint32_t)kTcTmemCols;
+    mma_tf32(d, a_hi, b_hi, idesc, 0);
+    mma_tf32(d, a_hi, b_lo, idesc, 1);
+    mma_tf32(d, a_lo, b_hi, idesc, 1);
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        full_addr + 8 * (uint32_t)(j & 1)));
+  };
+  if (tid == 0) {
+    if (WBULK && nitems > 0) mbar_wait(wbar_addr, 0);  // the resident W landed
+    if (nitems > 0) issue(0, 0, 0);
+    if (nitems > 1) issue(nch > 1 ? 0 : 1, nch > 1 ? 1 : 0, 1);
+  }
+  PI2_TC_TDECL
+  int64_t j = 0;
+  for (int64_t i = 0; i < nt; ++i) {
+    float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;
+    for (int c = 0; c < nch; ++c, ++j) {
+      const int lc = a.chunk_pad[ax][c];
+      const int nlo = SPLIT == 2 ? (lc >> 4) << 3 : lc;  // low warps: floor(half) in batches of 8
+      const int f0 = half ? nlo : 0, nf = half ? lc - nlo : nlo;
+      const uint32_t b = (uint32_t)(j & 1);
+      mbar_wait(full_addr + 8 * b, (uint32_t)((j >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // STREAM: this item's W slot is free again once its MMA completed: stage item j + 2's
+      if (STREAM && tid == 0 && j + 2 < nitems) load_w((c + 2) % nch, b);
+      PI2_TC_T(2);
+      tc_exp_span<VAR, STREAM, kTcChunk / SPLIT>(tmem_lane + b * (uint32_t)kTcTmemCols + (uint32_t)f0, lc, nf,
+                                             slv_base + (int64_t)c * kTcChunk + f0, den, num, m2, lv);
+      PI2_TC_T(3);
+      // features due before this item is released: tile t with t * nch - 2 == j
+      if (half == 0 && fnext < nt && fnext * nch - 2 == j) {
+        features(fnext, xn);
+        PI2_TC_T(5);
+        ++fnext;
+        if (fnext < nt) xn = load_x(fnext);
+        asm volatile("fence.proxy.async.shared::cta;");
+        PI2_TC_T(6);
+      }
+      // tile i done: the low half hands its moments to the high half, which reads them (and
+      // the row's stash) before releasing the item -- so neither slot can be overwritten
+      // before it is read -- and finalizes after
+      const bool tile_end = c == nch - 1;
+      float4 lo = make_float4(0.f, 0.f, 0.f, 0.f);
+      float2 pre = make_float2(0.f, 0.f);
+      if (SPLIT == 2 && tile_end) {
+        const int slot = (int)(i & 1);
+        const uint32_t pb = pready_addr + 8 * (uint32_t)(quarter * 2 + slot);
+        if (half == 0) {
+          part[slot * 128 + row_in_tile] = make_float4(__fadd_rn(den.x, den.y), __fadd_rn(num.x, num.y),
+                                                       __fadd_rn(m2.x, m2.y), 0.0f);
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(pb) : "memory");
+        } else {
+          mbar_wait(pb, (uint32_t)((i >> 1) & 1));
+          lo = part[slot * 128 + row_in_tile];
+          pre = stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (j + 2 < nitems) {  // buffer b is free once every warp got here: item j + 2 goes there
+        if (warp == 0) {
+          named_bar_sync(1 + (int)b, 128 * SPLIT);
+          PI2_TC_T(7);
+          if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int c2 = (c + 2) % nch;
+            issue(i + (c + 2) / nch, c2, j + 2);
+          }
+        } else {
+          named_bar_arrive(1 + (int)b, 128 * SPLIT);
+        }
+      }
+      PI2_TC_T(1);
+      if (SPLIT == 2 && tile_end && half == 1)
+        tc_finalize3<VAR>(a, h, ax, row_of(i), pre.x, pre.y, __fadd_rn(lo.x, __fadd_rn(den.x, den.y)),
+                          __fadd_rn(lo.y, __fadd_rn(num.x, num.y)), __fadd_rn(lo.z, __fadd_rn(m2.x, m2.y)));
+      if (SPLIT == 1 && tile_end) {
+        const float2 p = stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile];
+        tc_finalize3<VAR>(a, h, ax, row_of(i), p.x, p.y, __fadd_rn(den.x, den.y), __fadd_rn(num.x, num.y),
+                          __fadd_rn(m2.x, m2.y));
+      }
+      PI2_TC_T(0);
+    }
+  }
+  PI2_TC_T(4);
+  PI2_TC_TFLUSH
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTc3TmemCols));
+}
+
+// dynamic shared memory of lwpr_tc3_kernel (W or its ring + variances, then A, stash,
+// partials), padded so exactly kTc3CtasPerSm CTAs fit on an SM
+inline int tc3_smem_bytes(int64_t w_axis_floats, const void *fn) {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  const int need = (int)((w_axis_floats * 4 + 127) / 128 * 128 + kTc3ExtraBytes);
+  const int cap = 228 * 1024 / kTc3CtasPerSm - 1024 - (int)fa.sharedSizeBytes - 256;
+  return need > cap ? -1 : cap;
 }
 
 // ---- host: W operands of the tensor-core path ------------------------------

@@ -3,6 +3,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //          -I paper_1503_00330_b200/csrc -o lwpr_tc_test profiles/micro/lwpr_tc_test.cu
 #include <cstdio>
+#include <cstring>
 #include <algorithm>
 #include <vector>
 
@@ -11,6 +12,15 @@
 using namespace pi2;
 
 static uint64_t s_rng = 88172645463325252ull;
+static uint64_t fnv(const std::vector<float> &v, int64_t n) {  // bit hash of the first n floats
+  uint64_t h = 1469598103934665603ull;
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t b;
+    memcpy(&b, &v[i], 4);
+    h = (h ^ b) * 1099511628211ull;
+  }
+  return h;
+}
 static double urand() {
   s_rng ^= s_rng << 13; s_rng ^= s_rng >> 7; s_rng ^= s_rng << 17;
   return (s_rng >> 11) * (1.0 / 9007199254740992.0);
@@ -70,20 +80,25 @@ int main(int argc, char **argv) {
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
   int64_t lvmax = 0;
   for (int i = 0; i < 3; ++i) lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
-  auto *k2 = lwpr_tc_kernel<true, false>;
-  auto *k4 = lwpr_tc_kernel<false, false>;
-  int smem2 = tc_smem_bytes(wmax, (const void *)k2);
+  // TC3=1: the column-split double-buffered kernel (lwpr_tc3_kernel) instead of lwpr_tc_kernel
+  const bool tc3 = getenv("TC3") && atoi(getenv("TC3"));
+  auto *k2 = tc3 ? lwpr_tc3_kernel<true, false, false> : lwpr_tc_kernel<true, false>;
+  auto *k4 = tc3 ? lwpr_tc3_kernel<false, false, false> : lwpr_tc_kernel<false, false>;
+  auto smem_of = [&](int64_t wf, const void *fn) { return tc3 ? tc3_smem_bytes(wf, fn) : tc_smem_bytes(wf, fn); };
+  int smem2 = smem_of(wmax, (const void *)k2);
   const bool stream = smem2 < 0 || getenv("STREAM");
   if (stream) {  // W streamed per chunk
-    k2 = lwpr_tc_kernel<true, true>;
-    k4 = lwpr_tc_kernel<false, true>;
-    smem2 = tc_smem_bytes(2 * kTcWSlotFloats + lvmax, (const void *)k2);
+    k2 = tc3 ? lwpr_tc3_kernel<true, true, false> : lwpr_tc_kernel<true, true>;
+    k4 = tc3 ? lwpr_tc3_kernel<false, true, false> : lwpr_tc_kernel<false, true>;
+    smem2 = smem_of(2 * kTcWSlotFloats + lvmax, (const void *)k2);
   }
+  const int tc_threads = tc3 ? kTc3Threads : kTcThreads, tc_per_sm = tc3 ? kTc3CtasPerSm : kTcCtasPerSm;
+  printf("kernel %s\n", tc3 ? "lwpr_tc3_kernel" : "lwpr_tc_kernel");
   printf("W %s\n", stream ? "streamed" : "resident");
-  if (smem2 < 0) { printf("does not fit %d CTAs/SM\n", kTcCtasPerSm); return 1; }
+  if (smem2 < 0) { printf("does not fit %d CTAs/SM\n", tc_per_sm); return 1; }
   cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const unsigned g2 = (kTcCtasPerSm * sms) / 3 * 3;
+  const unsigned g2 = (tc_per_sm * sms) / 3 * 3;
   printf("CTAS %d CHUNK %d\n", PI2_TC_CTAS, PI2_TC_CHUNK);
   printf("rows %lld L %d: W %lld floats, lv %lld, smem tc %d B, chunks %d pad %d\n", (long long)rows, L,
          (long long)ta.w_floats, (long long)ta.lv_floats, smem2, ta.nchunks[0], ta.chunk_pad[0][0]);
@@ -91,14 +106,77 @@ int main(int argc, char **argv) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   float ms1, ms2;
   k1<<<g1, 128, smem1>>>(la);
-  k2<<<g2, kTcThreads, smem2>>>(ta);
+  k2<<<g2, tc_threads, smem2>>>(ta);
   cudaError_t err = cudaDeviceSynchronize();
   printf("first run: %s\n", cudaGetErrorString(err));
   if (err != cudaSuccess) return 2;
   cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k1<<<g1, 128, smem1>>>(la); cudaEventRecord(e1);
   cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
-  cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k2<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
+  cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k2<<<g2, tc_threads, smem2>>>(ta); cudaEventRecord(e1);
   cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+#ifdef PI2_TC_TRACE
+  {  // one traced launch: per SM sub-partition (hw warp slot % 4), time share with n warps in the exp phase
+    const int on = 1;
+    unsigned zero = 0;
+    void *tbuf;
+    cudaGetSymbolAddress(&tbuf, g_tc_trace);
+    cudaMemset(tbuf, 0, sizeof(unsigned long long) * 64 * kTcTraceCap);
+    cudaMemcpyToSymbol(g_tc_trace_n, &zero, 4);
+    cudaMemcpyToSymbol(g_tc_trace_on, &on, 4);
+    k2<<<g2, tc_threads, smem2>>>(ta);
+    cudaDeviceSynchronize();
+    const int off = 0;
+    cudaMemcpyToSymbol(g_tc_trace_on, &off, 4);
+    std::vector<unsigned long long> all(64 * kTcTraceCap), ev;
+    cudaMemcpy(all.data(), tbuf, all.size() * 8, cudaMemcpyDeviceToHost);
+    for (auto e : all)
+      if (e) ev.push_back(e);
+    const unsigned n = (unsigned)ev.size();
+    std::sort(ev.begin(), ev.end());
+    // per warp slot: last event clock; interval (last, now] is the phase that ended now
+    std::vector<long long> last(64, -1);
+    std::vector<int> inexp(4, 0);
+    std::vector<int> cur(64, -1);  // phase the warp is in (known only after its event) -- use end-labelled intervals
+    // build intervals
+    struct Iv { long long a, b; int w, ph; };
+    std::vector<Iv> iv;
+    for (auto e : ev) {
+      const long long c = (long long)(e >> 20);
+      const int w = (int)((e >> 4) & 63), ph = (int)(e & 15);
+      if (last[w] >= 0) iv.push_back({last[w], c, w, ph});
+      last[w] = c;
+    }
+    long long t0 = 1LL << 62, t1 = 0;
+    for (auto &v : iv) { t0 = std::min(t0, v.a); t1 = std::max(t1, v.b); }
+    for (int sp = 0; sp < 4; ++sp) {
+      std::vector<std::pair<long long, int>> d;
+      double ph_tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (auto &v : iv)
+        if (v.w % 4 == sp) {
+          ph_tot[v.ph] += (double)(v.b - v.a);
+          if (v.ph == 3) { d.push_back({v.a, 1}); d.push_back({v.b, -1}); }
+        }
+      std::sort(d.begin(), d.end());
+      double hist[9] = {0};
+      int k = 0; long long prev = t0;
+      for (auto &x : d) { hist[std::min(k, 8)] += (double)(x.first - prev); prev = x.first; k += x.second; }
+      hist[0] += (double)(t1 - prev);
+      const double T = (double)(t1 - t0);
+      printf("SMSP %d (%.0f clk): time with n warps in exp:", sp, T);
+      for (int i = 0; i < 6; ++i) printf(" %d:%.2f", i, hist[i] / T);
+      printf("   phase clk: ph0 %.0f ph1 %.0f mma %.0f exp %.0f ph5 %.0f ph6 %.0f ph7 %.0f\n", ph_tot[0], ph_tot[1], ph_tot[2], ph_tot[3], ph_tot[5], ph_tot[6], ph_tot[7]);
+    }
+    printf("events %u\n", n);
+    // timeline sample: every warp of SM 0, a window after the start
+    const long long w0 = getenv("TRACE_FROM") ? atoll(getenv("TRACE_FROM")) : 100000, w1 = w0 + 12000;
+    int shown = 0;
+    for (auto &v : iv)
+      if (v.a - t0 >= w0 && v.a - t0 < w1 && shown < 400) {
+        printf("  w%02d %7lld-%7lld ph%d (%lld)\n", v.w, v.a - t0, v.b - t0, v.ph, v.b - v.a);
+        ++shown;
+      }
+  }
+#endif
 #ifdef PI2_TC_PROF
   {
     unsigned long long pr[5];
@@ -125,6 +203,7 @@ int main(int argc, char **argv) {
          flops / (ms1 / 5) / 1e9, ms2 / 5 * 1e3, flops / (ms2 / 5) / 1e9);
   printf("max |dmean| %.3e (max |mean| %.2f), max rel dstd %.3e, nan/inf %lld\n", dm, mm, ds, (long long)bad);
   printf("sample: cc %f %f tc %f %f\n", a1[0], b1[0], a2[0], b2[0]);
+  printf("tc output hash: mean %016llx std %016llx\n", (unsigned long long)fnv(a2, rows * 3), (unsigned long long)fnv(b2, rows * 3));
   {  // mean only (M = 1 rollouts)
     auto *k3 = lwpr_kernel<kLayShared, false, 8>;
     cudaFuncSetAttribute((const void *)k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
@@ -132,15 +211,16 @@ int main(int argc, char **argv) {
     la.sd_out = nullptr;
     ta.sd_out = nullptr;
     k3<<<g1, 128, smem1>>>(la);
-    k4<<<g2, kTcThreads, smem2>>>(ta);
+    k4<<<g2, tc_threads, smem2>>>(ta);
     cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k3<<<g1, 128, smem1>>>(la); cudaEventRecord(e1);
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms1, e0, e1);
-    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k4<<<g2, kTcThreads, smem2>>>(ta); cudaEventRecord(e1);
+    cudaEventRecord(e0); for (int r = 0; r < 5; ++r) k4<<<g2, tc_threads, smem2>>>(ta); cudaEventRecord(e1);
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
     cudaMemcpy(a1.data(), m1, rows * 16, cudaMemcpyDeviceToHost);
     cudaMemcpy(a2.data(), m2, rows * 16, cudaMemcpyDeviceToHost);
     double dm0 = 0;
     for (int64_t i = 0; i < rows * 4; ++i) dm0 = fmax(dm0, fabs(a1[i] - a2[i]));
+    printf("tc mean-only output hash: %016llx\n", (unsigned long long)fnv(a2, rows * 3));
     printf("mean-only  cuda-core: %8.1f us   tensor-core: %8.1f us   max |dmean| %.3e   (%s)\n", ms1 / 5 * 1e3,
            ms2 / 5 * 1e3, dm0, cudaGetErrorString(cudaDeviceSynchronize()));
   }
