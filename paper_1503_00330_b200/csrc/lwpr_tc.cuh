@@ -589,277 +589,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const
 }
 
 
-// ---- column-split, TMEM double-buffered schedule (lwpr_tc3_kernel) ----------
-// Phase traces of lwpr_tc_kernel (micro/tc_trace_b200.txt) show each warp in its exp
-// phase only ~36 % of the time (CTA barrier 24 %, MMA wait 22 %, features + finalize
-// 17 %): the next chunk's MMA can only start once the slowest warp has read the
-// current chunk out of the CTA's single TMEM buffer, and it takes ~450-600 clocks
-// (micro/mma_lat_b200.txt).  So only ~1.4 warps per SM sub-partition feed MUFU on
-// average, while the exp loop alone reaches 61 % of MUFU peak with one warp and 77 % with
-// four (micro/exp_loop_rate_b200.txt).  A split barrier alone does not help
-// (micro/lwpr_tc_splitbar_b200.txt): the critical path runs through the MMA.
-//
-// Here a CTA has 8 warps and 256 TMEM columns = two chunk buffers (2 CTAs per SM, the
-// same 16 warps and 512 columns per SM).  Warps w and w + 4 own the same 32 rows (TMEM
-// lanes 32 (w % 4) ..) and split every chunk's fields (w: the first half, rounded down to
-// 8, w + 4: the rest).  Item j = (tile, chunk) lives in buffer j & 1; the MMA of item
-// j + 2 is issued by thread 0 as soon as every warp has read item j (a named barrier:
-// warp 0 bar.sync, the others bar.arrive), so it runs while the warps are in item
-// j + 1's exp phase and no warp waits for an MMA unless it runs a whole item ahead.
-// The low warps also write the features (tile t's, into A[t % 3], before item
-// t * nch - 2 is released) and hand their partial moments to the high warps through
-// shared memory + an mbarrier; the high warps finalize.  Per row, den / num / m2 are the
-// sums of the two halves' sums (a different association than lwpr_tc_kernel: equal
-// within rounding).
-#ifndef PI2_TC3_SPLIT
-#define PI2_TC3_SPLIT 1
-#endif
-constexpr int kTc3Threads = 128 * PI2_TC3_SPLIT;
-constexpr int kTc3CtasPerSm = 2;
-constexpr int kTc3TmemCols = 2 * kTcTmemCols;  // two chunk buffers
-constexpr int kTc3ABuf = 3;
-constexpr int kTc3Stash = 4;  // (g(x), probe) slots: tile t in t % 4
-constexpr int kTc3ExtraBytes = kTc3ABuf * kTcABytes + kTc3Stash * 128 * 8 + 2 * 128 * 16;  // A, stash, partials
-
-template <bool VAR>
-__device__ __forceinline__ void tc_finalize3(const LwprTcArgs &a, const AxisHeader &h, int ax, int64_t row, float gx,
-                                             float fin, float dn, float nm, float m2) {
-  if (row >= a.rows) return;
-  float mean, var = 0.0f;
-  if (dn >= kSlowDen && dn <= 3.0e38f && isfinite(fin)) {
-    const float rd = rcp_fma(dn);
-    const float mp = __fmul_rn(nm, rd);
-    mean = __fadd_rn(gx, mp);
-    if (VAR) var = fmaxf(__fsub_rn(__fmul_rn(m2, rd), __fmul_rn(mp, mp)), 0.0f);
-  } else {  // rare: the centred inputs again, for the exact path
-    const float4 x = __ldcg(a.x + row);
-    const float4 xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]),
-                                  __fsub_rn(x.w, h.mu[3]));
-    const float2 mv = lwpr_row_exact<kLayShared>(a.params + h.offset, h.num_fields, xt, shared_qrow(h, xt), gx);
-    mean = mv.x;
-    var = mv.y;
-  }
-  a.mean_out[ax * a.plane + row] = mean;  // a warp writes 128 contiguous bytes
-  if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
-}
-
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// SPLIT = 2: 8 warps, each chunk's fields split between warps w and w + 4 (above).
-// SPLIT = 1: 4 warps, each reads its rows' whole chunk: an item's exp phase (64 fields)
-// outlasts the MMA of the item two ahead, which the split halves do not.
-template <bool VAR, bool STREAM, bool WBULK, int SPLIT = PI2_TC3_SPLIT>
-__global__ void __launch_bounds__(128 * SPLIT, kTc3CtasPerSm) lwpr_tc3_kernel(const __grid_constant__ LwprTcArgs a) {
-  extern __shared__ __align__(128) uint8_t tsm[];
-  __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t full[2];    // MMA of the item in buffer b complete
-  __shared__ __align__(8) uint64_t wbar[2];    // STREAM: W slot s holds its chunk; WBULK: resident W landed
-  __shared__ __align__(8) uint64_t pready[8];  // quarter q, slot s: low warp's partial moments of a tile written
-  const int ax = (int)(blockIdx.x % 3);
-  const int nch = a.nchunks[ax];
-  const int64_t wbeg = a.axis_off[ax], wend = ax < 2 ? a.axis_off[ax + 1] : a.w_floats;
-  const int64_t nlv = (int64_t)nch * kTcChunk;
-  const int64_t wfl = STREAM ? 2 * kTcWSlotFloats : wend - wbeg;
-  float *sw = reinterpret_cast<float *>(tsm);
-  float *slv_base = sw + wfl;
-  uint8_t *sa = tsm + (((wfl + nlv) * 4 + 127) / 128) * 128;                // kTc3ABuf A operands
-  float2 *stash = reinterpret_cast<float2 *>(sa + kTc3ABuf * kTcABytes);       // (g(x), probe) per A slot and row
-  float4 *part = reinterpret_cast<float4 *>(stash + kTc3Stash * 128);         // low half's moments per slot and row
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int half = SPLIT == 2 ? warp >> 2 : 0, quarter = warp & 3;
-  const int row_in_tile = quarter * 32 + lane;
-
-  if (!STREAM && !WBULK)
-    for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
-      reinterpret_cast<float4 *>(sw)[i] = __ldg(reinterpret_cast<const float4 *>(a.w + wbeg) + i);
-  for (int64_t i = tid; i < nlv; i += blockDim.x) slv_base[i] = __ldg(a.w + a.lv_off[ax] + i);
-  const uint32_t wbar_addr = (uint32_t)__cvta_generic_to_shared(&wbar[0]);
-  const uint32_t full_addr = (uint32_t)__cvta_generic_to_shared(&full[0]);
-  const uint32_t pready_addr = (uint32_t)__cvta_generic_to_shared(&pready[0]);
-  const uint32_t sw_addr = (uint32_t)__cvta_generic_to_shared(sw);
-  auto load_w = [&](int c, uint32_t slot) {  // thread 0: chunk c's W into ring slot `slot`
-    const uint32_t bytes = (uint32_t)(2 * 2 * a.chunk_pad[ax][c] * 8 * 4);
-    const uint32_t bar = wbar_addr + 8 * slot;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            sw_addr + slot * (uint32_t)(kTcWSlotFloats * 4)),
-        "l"(a.w + wbeg + a.chunk_woff[ax][c]), "r"(bytes), "r"(bar)
-        : "memory");
-  };
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
-                 "n"(kTc3TmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  const AxisHeader &h = a.axis[ax];
-  const int64_t ntiles = (a.rows + 127) / 128, last = a.rows - 1;
-  const int64_t tstride = gridDim.x / 3, tile0 = blockIdx.x / 3;
-  const int64_t nt = tile0 < ntiles ? (ntiles - tile0 + tstride - 1) / tstride : 0;  // tiles of this CTA
-  const int64_t nitems = nt * nch;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_addr));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_addr + 8));
-    for (int i = 0; i < 8; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(pready_addr + 8 * i));
-    if (STREAM || WBULK) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr + 8));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    if (STREAM) {
-      if (nitems > 0) load_w(0, 0);
-      if (nitems > 1) load_w(1 % nch, 1);
-    } else if (WBULK && nt > 0) {
-      const uint32_t bytes = (uint32_t)((wend - wbeg) * 4);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wbar_addr), "r"(bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sw_addr),
-          "l"(a.w + wbeg), "r"(bytes), "r"(wbar_addr)
-          : "memory");
-    }
-  }
-  auto row_of = [&](int64_t i) { return (tile0 + i * tstride) * 128 + row_in_tile; };
-  auto load_x = [&](int64_t i) {
-    const int64_t r = row_of(i);
-    return __ldcg(a.x + (r < last ? r : last));
-  };
-  // low warps: tile i's features -> A[i % 3], its g(x) and finiteness probe -> stash
-  auto features = [&](int64_t i, float4 x) {
-    float4 xt;
-    float q;
-    tc_features(h, x, sa + (int)(i % kTc3ABuf) * kTcABytes, row_in_tile, xt, q);
-    const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
-    stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile] =
-        make_float2(gx, __fadd_rn(__fadd_rn(xt.x, xt.y), __fadd_rn(__fadd_rn(xt.z, xt.w), q)));
-  };
-  // x comes from the attitude kernel: wait for it, then coherent loads (see lwpr_tc_body)
-  pdl_wait();
-  int64_t fnext = 0;  // next tile whose features the low warps write
-  float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (half == 0) {
-    const int64_t pro = nch == 1 ? 2 : 1;  // tiles staged before the first MMA  // tiles staged before the first MMA
-    for (; fnext < pro && fnext < nt; ++fnext) features(fnext, load_x(fnext));
-    if (fnext < nt) xn = load_x(fnext);
-  }
-  asm volatile("fence.proxy.async.shared::cta;");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
-  const uint32_t tmem_lane = tmem + ((uint32_t)(quarter * 32) << 16);
-  const uint32_t sa_addr0 = (uint32_t)__cvta_generic_to_shared(sa);
-  // thread 0: the 3 MMAs of item j = (tile i, chunk c) into buffer j & 1
-  auto issue = [&](int64_t i, int c, int64_t j) {
-    const int lc = a.chunk_pad[ax][c];
-    const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
-    const uint32_t sa_addr = sa_addr0 + (uint32_t)(i % kTc3ABuf) * kTcABytes;
-    const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
-    if (STREAM) mbar_wait(wbar_addr + 8 * (uint32_t)(j & 1), (uint32_t)((j >> 1) & 1));  // its W landed
-    const uint32_t wb = STREAM ? sw_addr + (uint32_t)(j & 1) * (uint32_t)(kTcWSlotFloats * 4)
-                               : sw_addr + (uint32_t)(a.chunk_woff[ax][c] * 4);
-    const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
-    const uint32_t d = tmem + (uint32_t)(j & 1) * (uint32_t)kTcTmemCols;
-    mma_tf32(d, a_hi, b_hi, idesc, 0);
-    mma_tf32(d, a_hi, b_lo, idesc, 1);
-    mma_tf32(d, a_lo, b_hi, idesc, 1);
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-        full_addr + 8 * (uint32_t)(j & 1)));
-  };
-  if (tid == 0) {
-    if (WBULK && nitems > 0) mbar_wait(wbar_addr, 0);  // the resident W landed
-    if (nitems > 0) issue(0, 0, 0);
-    if (nitems > 1) issue(nch > 1 ? 0 : 1, nch > 1 ? 1 : 0, 1);
-  }
-  PI2_TC_TDECL
-  int64_t j = 0;
-  for (int64_t i = 0; i < nt; ++i) {
-    float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;
-    for (int c = 0; c < nch; ++c, ++j) {
-      const int lc = a.chunk_pad[ax][c];
-      const int nlo = SPLIT == 2 ? (lc >> 4) << 3 : lc;  // low warps: floor(half) in batches of 8
-      const int f0 = half ? nlo : 0, nf = half ? lc - nlo : nlo;
-      const uint32_t b = (uint32_t)(j & 1);
-      mbar_wait(full_addr + 8 * b, (uint32_t)((j >> 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      // STREAM: this item's W slot is free again once its MMA completed: stage item j + 2's
-      if (STREAM && tid == 0 && j + 2 < nitems) load_w((c + 2) % nch, b);
-      PI2_TC_T(2);
-      tc_exp_span<VAR, STREAM, kTcChunk / SPLIT>(tmem_lane + b * (uint32_t)kTcTmemCols + (uint32_t)f0, lc, nf,
-                                             slv_base + (int64_t)c * kTcChunk + f0, den, num, m2, lv);
-      PI2_TC_T(3);
-      // features due before this item is released: tile t with t * nch - 2 == j
-      if (half == 0 && fnext < nt && fnext * nch - 2 == j) {
-        features(fnext, xn);
-        PI2_TC_T(5);
-        ++fnext;
-        if (fnext < nt) xn = load_x(fnext);
-        asm volatile("fence.proxy.async.shared::cta;");
-        PI2_TC_T(6);
-      }
-      // tile i done: the low half hands its moments to the high half, which reads them (and
-      // the row's stash) before releasing the item -- so neither slot can be overwritten
-      // before it is read -- and finalizes after
-      const bool tile_end = c == nch - 1;
-      float4 lo = make_float4(0.f, 0.f, 0.f, 0.f);
-      float2 pre = make_float2(0.f, 0.f);
-      if (SPLIT == 2 && tile_end) {
-        const int slot = (int)(i & 1);
-        const uint32_t pb = pready_addr + 8 * (uint32_t)(quarter * 2 + slot);
-        if (half == 0) {
-          part[slot * 128 + row_in_tile] = make_float4(__fadd_rn(den.x, den.y), __fadd_rn(num.x, num.y),
-                                                       __fadd_rn(m2.x, m2.y), 0.0f);
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(pb) : "memory");
-        } else {
-          mbar_wait(pb, (uint32_t)((i >> 1) & 1));
-          lo = part[slot * 128 + row_in_tile];
-          pre = stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile];
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      if (j + 2 < nitems) {  // buffer b is free once every warp got here: item j + 2 goes there
-        if (warp == 0) {
-          named_bar_sync(1 + (int)b, 128 * SPLIT);
-          PI2_TC_T(7);
-          if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const int c2 = (c + 2) % nch;
-            issue(i + (c + 2) / nch, c2, j + 2);
-          }
-        } else {
-          named_bar_arrive(1 + (int)b, 128 * SPLIT);
-        }
-      }
-      PI2_TC_T(1);
-      if (SPLIT == 2 && tile_end && half == 1)
-        tc_finalize3<VAR>(a, h, ax, row_of(i), pre.x, pre.y, __fadd_rn(lo.x, __fadd_rn(den.x, den.y)),
-                          __fadd_rn(lo.y, __fadd_rn(num.x, num.y)), __fadd_rn(lo.z, __fadd_rn(m2.x, m2.y)));
-      if (SPLIT == 1 && tile_end) {
-        const float2 p = stash[(int)(i & (kTc3Stash - 1)) * 128 + row_in_tile];
-        tc_finalize3<VAR>(a, h, ax, row_of(i), p.x, p.y, __fadd_rn(den.x, den.y), __fadd_rn(num.x, num.y),
-                          __fadd_rn(m2.x, m2.y));
-      }
-      PI2_TC_T(0);
-    }
-  }
-  PI2_TC_T(4);
-  PI2_TC_TFLUSH
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTc3TmemCols));
-}
-
-// dynamic shared memory of lwpr_tc3_kernel (W or its ring + variances, then A, stash,
-// partials), padded so exactly kTc3CtasPerSm CTAs fit on an SM
-inline int tc3_smem_bytes(int64_t w_axis_floats, const void *fn) {
-  cudaFuncAttributes fa{};
-  cudaFuncGetAttributes(&fa, fn);
-  const int need = (int)((w_axis_floats * 4 + 127) / 128 * 128 + kTc3ExtraBytes);
-  const int cap = 228 * 1024 / kTc3CtasPerSm - 1024 - (int)fa.sharedSizeBytes - 256;
-  return need > cap ? -1 : cap;
-}
+// Schedules tried against this one (bitwise equal, all slower at C2 size): a split
+// barrier (micro/lwpr_tc_splitbar_b200.txt), TMEM double buffers with every warp doing
+// its own features (micro/lwpr_tc3_dbuf_b200.txt), and warp-specialised exp / producer
+// warps with 2-4 TMEM buffers (micro/lwpr_tcws_b200.txt, patch micro/lwpr_tcws.patch).
 
 // ---- host: W operands of the tensor-core path ------------------------------
 // Same fold as fold_axis(kLayShared) in float64, split into tf32 hi + lo

@@ -80,20 +80,16 @@ int main(int argc, char **argv) {
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
   int64_t lvmax = 0;
   for (int i = 0; i < 3; ++i) lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
-  // TC3=1: the column-split double-buffered kernel (lwpr_tc3_kernel) instead of lwpr_tc_kernel
-  const bool tc3 = getenv("TC3") && atoi(getenv("TC3"));
-  auto *k2 = tc3 ? lwpr_tc3_kernel<true, false, false> : lwpr_tc_kernel<true, false>;
-  auto *k4 = tc3 ? lwpr_tc3_kernel<false, false, false> : lwpr_tc_kernel<false, false>;
-  auto smem_of = [&](int64_t wf, const void *fn) { return tc3 ? tc3_smem_bytes(wf, fn) : tc_smem_bytes(wf, fn); };
-  int smem2 = smem_of(wmax, (const void *)k2);
+  auto *k2 = lwpr_tc_kernel<true, false>;
+  auto *k4 = lwpr_tc_kernel<false, false>;
+  int smem2 = tc_smem_bytes(wmax, (const void *)k2);
   const bool stream = smem2 < 0 || getenv("STREAM");
   if (stream) {  // W streamed per chunk
-    k2 = tc3 ? lwpr_tc3_kernel<true, true, false> : lwpr_tc_kernel<true, true>;
-    k4 = tc3 ? lwpr_tc3_kernel<false, true, false> : lwpr_tc_kernel<false, true>;
-    smem2 = smem_of(2 * kTcWSlotFloats + lvmax, (const void *)k2);
+    k2 = lwpr_tc_kernel<true, true>;
+    k4 = lwpr_tc_kernel<false, true>;
+    smem2 = tc_smem_bytes(2 * kTcWSlotFloats + lvmax, (const void *)k2);
   }
-  const int tc_threads = tc3 ? kTc3Threads : kTcThreads, tc_per_sm = tc3 ? kTc3CtasPerSm : kTcCtasPerSm;
-  printf("kernel %s\n", tc3 ? "lwpr_tc3_kernel" : "lwpr_tc_kernel");
+  const int tc_threads = kTcThreads, tc_per_sm = kTcCtasPerSm;
   printf("W %s\n", stream ? "streamed" : "resident");
   if (smem2 < 0) { printf("does not fit %d CTAs/SM\n", tc_per_sm); return 1; }
   cudaFuncSetAttribute((const void *)k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
