@@ -246,6 +246,12 @@ int pi2_profile_evaluate(pi2_ctx *ctx, const double *state, const double *plan, 
 #define PI2_LWPR_CUDA_CORES 0
 #define PI2_LWPR_TENSOR_CORES 1
 int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double *mufu_share);
+/* Whether this context's device-noise iterations run the fused step kernel
+ * (attitude + LWPR + rollout/cost in one kernel, csrc/fused.cuh; opt-in with
+ * the environment variable PI2_FUSED=1 at pi2_create, and only for eligible
+ * models, costs and sizes): *sub_rollouts_out = its per-thread sub-rollout
+ * template (1, 2 or 4), 0 when the unfused kernels run.  Introspection. */
+int pi2_fused_step(pi2_ctx *ctx, int32_t *sub_rollouts_out);
 
 /* ---- noise / LWPR building blocks ------------------------------------- */
 /* Device noise for stream (seed, stream_id, cycle, iteration): control

@@ -84,6 +84,7 @@ _SIGNATURES = {
     "pi2_profile_iteration": (C.c_int, [_P, C.POINTER(OptimizeArgs), C.c_int32, _P]),
     "pi2_profile_evaluate": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, _P]),
     "pi2_lwpr_kernel": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "pi2_fused_step": (C.c_int, [_P, _P]),
     "pi2_device_noise": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, _P, _P]),
     "pi2_lwpr_predict": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P, _P]),
 }

@@ -298,11 +298,10 @@ __device__ __forceinline__ void tc_features(const AxisHeader &h, float4 x, uint8
   }
 }
 
-// mean / std of one row from its moments (exact path when the normaliser underflowed)
+// (mean, std) of one row from its moments (exact path when the normaliser underflowed)
 template <bool VAR>
-__device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeader &h, int ax, int64_t row, float4 xt,
-                                            float q, float dn, float nm, float m2, float lv) {
-  if (row >= a.rows) return;
+__device__ __forceinline__ float2 tc_mean_sd(const LwprTcArgs &a, const AxisHeader &h, float4 xt, float q, float dn,
+                                             float nm, float m2, float lv) {
   const float gx = fmaf(h.gs[3], xt.w, fmaf(h.gs[2], xt.z, fmaf(h.gs[1], xt.y, fmaf(h.gs[0], xt.x, h.g0))));
   float mean, var = 0.0f;
   // fast path: a normal normaliser and finite inputs (non-finite rows follow the
@@ -317,8 +316,17 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
     mean = mv.x;
     var = mv.y;
   }
-  a.mean_out[ax * a.plane + row] = mean;  // a warp writes 128 contiguous bytes
-  if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var;
+  return make_float2(mean, VAR ? (a.sqrt_out ? (var >= 1.17549435e-38f && var <= 3.40282347e38f ? sqrt_fma(var) : sqrtf(var)) : var)
+                                : 0.0f);
+}
+
+template <bool VAR>
+__device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeader &h, int ax, int64_t row, float4 xt,
+                                            float q, float dn, float nm, float m2, float lv) {
+  if (row >= a.rows) return;
+  const float2 ms = tc_mean_sd<VAR>(a, h, xt, q, dn, nm, m2, lv);
+  a.mean_out[ax * a.plane + row] = ms.x;  // a warp writes 128 contiguous bytes
+  if (VAR && a.sd_out) a.sd_out[ax * a.plane + row] = ms.y;
 }
 
 // The exp phase of nf (multiple of 8) fields of this warp's 32 rows, read from TMEM

@@ -20,6 +20,7 @@
 #include "fold.h"
 #include "kernels.cuh"
 #include "lwpr_tc.cuh"
+#include "fused.cuh"
 
 using namespace pi2;
 
@@ -55,6 +56,7 @@ struct pi2_ctx {
   bool uva = false;        // pinned host memory is device-accessible (unified addressing)
   bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
   int partials_split = 1;  // partials_split_kernel: 0 never, 1 when few (chunk, t) warps, 2 always
+  int fused = 0;           // device-noise iterations through fused_step_kernel when eligible (PI2_FUSED=1; slower, see DESIGN)
   int64_t wide_max_k = kWideMaxK;  // attitude/rollout use a warp per rollout up to this K (PI2_WIDE_MAX_K)
   int64_t tc_bulk_max_tiles = kTcBulkMaxTiles;  // WBULK LWPR up to this many tiles per CTA (PI2_TC_BULK_MAX_TILES)
   LwprTcArgs tc{};
@@ -441,6 +443,71 @@ int stage_plan(pi2_ctx *ctx, const double *plan, cudaStream_t st) {
   return PI2_OK;
 }
 
+// The fused kernel (fused.cuh) runs a device-noise iteration's rollouts when the model
+// is the hybrid LWPR on the tensor cores (shared metric, <= kFusedMaxChunks chunks per
+// axis), the cost is the navigation cost, K is past the latency regime and the
+// sub-rollouts fit (S <= kFusedMaxM); its shared memory must leave room for
+// kTcCtasPerSm CTAs.  Returns the sub-rollout template (1, 2, 4) or 0.
+int fused_mm(pi2_ctx *ctx) {
+  if (!ctx->fused || ctx->model != PI2_MODEL_HYBRID_LWPR || ctx->cost.kind != PI2_COST_NAVIGATION) return 0;
+  if (ensure_params(ctx) != PI2_OK || !ctx->tc_ok || ctx->K <= ctx->wide_max_k) return 0;
+  const bool var = spread(ctx) || penalty(ctx);
+  if (!tc_wanted(ctx, var)) return 0;
+  for (int i = 0; i < 3; ++i)
+    if (ctx->tc.nchunks[i] > kFusedMaxChunks) return 0;
+  const int S = spread(ctx) ? ctx->M : 1;
+  const int mm = S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : 0));
+  if (!mm) return 0;
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, (const void *)fused_step_kernel<true, 4>);  // static shared memory: same for all
+  const int cap = 228 * 1024 / kTcCtasPerSm - 1024 - (int)fa.sharedSizeBytes - 256;
+  return fused_smem_bytes(ctx->tc.nchunks, mm) <= cap ? mm : 0;
+}
+
+template <bool VAR, int MM>
+int launch_fused_t(pi2_ctx *ctx, const FusedArgs &f, cudaStream_t st, bool pdl) {
+  auto *fn = fused_step_kernel<VAR, MM>;
+  const int smem = fused_smem_bytes(f.tc.nchunks, MM);
+  TRY(set_smem(ctx, fn, smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int64_t blocks = (f.K + kTcThreads - 1) / kTcThreads;
+  const int64_t grid = std::min<int64_t>((int64_t)kTcCtasPerSm * sms, blocks);
+  TRY(launch_pdl_if(pdl, ctx, fn, dim3((unsigned)grid), dim3(kTcThreads), smem, st, f));
+  CU(cudaGetLastError());
+  return PI2_OK;
+}
+
+int launch_fused(pi2_ctx *ctx, int mm, int iteration, double *costs, uint8_t *crash, cudaStream_t st, bool pdl) {
+  FusedArgs f{};
+  f.tc = ctx->tc;
+  f.tc.params = ctx->d_params;
+  for (int i = 0; i < 3; ++i) f.tc.axis[i] = ctx->hdr[i];
+  f.tc.rows = ctx->K * ctx->N;
+  f.tc.sqrt_out = 1;
+  f.sa = ctx->d_args;
+  f.plan = ctx->d_plan;
+  f.iteration = iteration;
+  f.K = ctx->K;
+  f.k_off = ctx->dims.rollout_offset;
+  f.N = ctx->N;
+  f.M = ctx->M;
+  f.spread = spread(ctx) ? 1 : 0;
+  f.penalty = penalty(ctx) ? 1 : 0;
+  f.dp = ctx->dp;
+  f.zout = ctx->d_z;
+  f.qbuf = reinterpret_cast<float *>(ctx->d_lw);  // the LWPR planes are not used on this path
+  f.costs = costs;
+  f.crash = crash;
+  const bool var = f.spread || f.penalty;
+  if (var) {
+    if (mm == 1) return launch_fused_t<true, 1>(ctx, f, st, pdl);
+    if (mm == 2) return launch_fused_t<true, 2>(ctx, f, st, pdl);
+    return launch_fused_t<true, 4>(ctx, f, st, pdl);
+  }
+  return launch_fused_t<false, 1>(ctx, f, st, pdl);
+}
+
 // rollouts of one iteration: attitude -> LWPR -> rollout/cost
 // att_pdl: the attitude kernel may be a programmatic dependent launch (its stream
 // predecessor is a kernel whose outputs it reads only after pdl_wait)
@@ -449,6 +516,16 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
                     bool att_pdl = false) {
   const int64_t K = ctx->K;
   const int N = ctx->N;
+  if (!noise_dev && !dyn_dev) {  // device noise: the fused kernel when eligible
+    const int mm = fused_mm(ctx);
+    if (mm) {
+      if (ev) {  // profiling: the attitude and LWPR stages are empty, the whole kernel is "rollout"
+        CU(cudaEventRecord(ev[1], st));
+        CU(cudaEventRecord(ev[2], st));
+      }
+      return launch_fused(ctx, mm, iteration, costs, crash, st, att_pdl);
+    }
+  }
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
   const int psmem = 4 * N * (int)sizeof(double);
   if (K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
@@ -642,6 +719,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if (const char *e = getenv("PI2_PARTIALS_SPLIT")) ctx->partials_split = std::atoi(e);
   if (const char *e = getenv("PI2_WIDE_MAX_K")) ctx->wide_max_k = std::atoll(e);
   if (const char *e = getenv("PI2_TC_BULK_MAX_TILES")) ctx->tc_bulk_max_tiles = std::atoll(e);
+  if (const char *e = getenv("PI2_FUSED")) ctx->fused = std::atoi(e);
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
@@ -1084,6 +1162,15 @@ int pi2_lwpr_kernel(pi2_ctx *ctx, int32_t variance, int32_t *kernel_out, double 
   return PI2_OK;
 }
 
+int pi2_fused_step(pi2_ctx *ctx, int32_t *sub_rollouts_out) {
+  TRY(check_ready(ctx));
+  if (!sub_rollouts_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
+  TRY(bind(ctx));
+  TRY(ensure_params(ctx));
+  *sub_rollouts_out = fused_mm(ctx);
+  return PI2_OK;
+}
+
 int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms) {
   TRY(check_ready(ctx));
   TRY(bind(ctx));
@@ -1278,3 +1365,19 @@ int pi2_lwpr_predict(pi2_ctx *ctx, int32_t axis, int64_t rows, const float *X, f
 }
 
 }  // extern "C"
+
+#ifdef PI2_TC_TRACE
+// experiments only (trace builds, not in include/pi2rh.h): arm the phase tracer / read it
+extern "C" int pi2_debug_trace_arm(int on) {
+  const unsigned zero = 0;
+  void *buf = nullptr;
+  cudaGetSymbolAddress(&buf, pi2::g_tc_trace);
+  cudaMemset(buf, 0, sizeof(unsigned long long) * 64 * pi2::kTcTraceCap);
+  cudaMemcpyToSymbol(pi2::g_tc_trace_n, &zero, 4);
+  cudaMemcpyToSymbol(pi2::g_tc_trace_on, &on, 4);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -1;
+}
+extern "C" int pi2_debug_trace_read(unsigned long long *out) {  // 64 * kTcTraceCap entries
+  return cudaMemcpyFromSymbol(out, pi2::g_tc_trace, sizeof(unsigned long long) * 64 * pi2::kTcTraceCap) == cudaSuccess ? 0 : -1;
+}
+#endif
