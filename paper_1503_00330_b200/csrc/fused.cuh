@@ -280,9 +280,14 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) fused_step_kernel(co
         mbar_wait(wbar_addr + 8 * (nw & 1), (nw >> 1) & 1);  // this chunk's W landed
         const uint32_t wb = sw_addr + (nw & 1) * (uint32_t)(kTcWSlotFloats * 4);
         const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
+#if PI2_TC_PACK2
+        mma_tf32(tmem, a_hi, b_hi, idesc, 0);  // A1 . B1
+        mma_tf32(tmem, a_lo, b_lo, idesc, 1);  // A2 . B2
+#else
         mma_tf32(tmem, a_hi, b_hi, idesc, 0);
         mma_tf32(tmem, a_hi, b_lo, idesc, 1);
         mma_tf32(tmem, a_lo, b_hi, idesc, 1);
+#endif
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar_addr));
       }
       PI2_TC_T(8);

@@ -213,6 +213,12 @@ __device__ __forceinline__ void tc_trace(int slot, int &n, int i) {
 #define PI2_TC_LD16 1
 #endif
 
+// 3xTF32 as TWO MMAs per chunk instead of three: the same product terms hi.hi + hi.lo +
+// lo.hi rearranged along K (A1 = [x~hi, 1, 1, q~hi, q~lo] . B1 = [Whi, A0hi, A0lo, 1, 1] and
+// A2 = [x~hi, x~lo] . B2 = [Wlo, Whi]); operands keep their sizes
+#ifndef PI2_TC_PACK2
+#define PI2_TC_PACK2 1
+#endif
 #ifndef PI2_TC_POLY_VAR
 #define PI2_TC_POLY_VAR 0   // field pairs (of 4 per 8-field batch) whose 2^x runs on the FMA pipe:
                             // the variance loop slows down with any (1: 436 -> 456 us at L=100), the
@@ -282,13 +288,27 @@ __device__ __forceinline__ void tc_fields8(const uint32_t *lg, const uint32_t *y
 __device__ __forceinline__ void tc_features(const AxisHeader &h, float4 x, uint8_t *sa, int r, float4 &xt, float &q) {
   xt = make_float4(__fsub_rn(x.x, h.mu[0]), __fsub_rn(x.y, h.mu[1]), __fsub_rn(x.z, h.mu[2]), __fsub_rn(x.w, h.mu[3]));
   q = shared_qrow(h, xt);
+  float hi[8], lo[8];  // PI2_TC_PACK2: the A1 | A2 operands of the two-MMA form; else the tf32 hi | lo split
+#if PI2_TC_PACK2
+  const float x4[4] = {xt.x, xt.y, xt.z, xt.w};
+  const float qh = tf32_rna(q);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    hi[k] = lo[k] = tf32_rna(x4[k]);
+    lo[4 + k] = tf32_rna(__fsub_rn(x4[k], hi[k]));
+  }
+  hi[4] = 1.0f;
+  hi[5] = 1.0f;
+  hi[6] = qh;
+  hi[7] = tf32_rna(__fsub_rn(q, qh));
+#else
   const float f[8] = {xt.x, xt.y, xt.z, xt.w, 1.0f, q, 0.0f, 0.0f};
-  float hi[8], lo[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     hi[k] = tf32_rna(f[k]);
     lo[k] = tf32_rna(__fsub_rn(f[k], hi[k]));
   }
+#endif
   // k = 0..3 and 4..7 of a row are 16 contiguous bytes each in the K-major layout:
   // 4 conflict-free 128-bit stores instead of 16 4-way-conflicted 32-bit ones
 #pragma unroll
@@ -530,9 +550,14 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
         if (STREAM) mbar_wait(wbar_addr + 8 * (nw & 1), (nw >> 1) & 1);  // this chunk's W landed
         const uint32_t wb = STREAM ? sw_addr + (nw & 1) * (uint32_t)(kTcWSlotFloats * 4) : sw_addr + (uint32_t)(woff * 4);
         const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
+#if PI2_TC_PACK2
+        mma_tf32(tmem, a_hi, b_hi, idesc, 0);  // A1 . B1
+        mma_tf32(tmem, a_lo, b_lo, idesc, 1);  // A2 . B2
+#else
         mma_tf32(tmem, a_hi, b_hi, idesc, 0);
         mma_tf32(tmem, a_hi, b_lo, idesc, 1);
         mma_tf32(tmem, a_lo, b_hi, idesc, 1);
+#endif
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             mbar_addr));
         // the other slot held chunk nw - 1, whose MMA completed before this chunk's barrier
@@ -665,16 +690,39 @@ inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, Lwpr
       const int lc = (n + 7) / 8 * 8;
       ta.chunk_pad[ax][c] = lc;
       ta.chunk_woff[ax][c] = (int)(w_floats - ta.axis_off[ax]);
+      // hi / lo: the B operands of the MMAs (PI2_TC_PACK2: B1 | B2, else the tf32 split)
       std::vector<float> hi(2 * lc * 8, 0.0f), lo(2 * lc * 8, 0.0f);
-      auto put = [&](int r, int k, double v) {
-        const float f = (float)v, fh = host_tf32_rna(f);
-        hi[umma_kmajor_off(r, k) / 4] = fh;
-        lo[umma_kmajor_off(r, k) / 4] = host_tf32_rna(f - fh);
+      auto at = [&](int r, int k) { return (size_t)(umma_kmajor_off(r, k) / 4); };
+      // row r: slopes w[4] on x~, constant c, q~ coefficient qc
+      auto row = [&](int r, const double *w, double c, double qc) {
+#if PI2_TC_PACK2
+        for (int i = 0; i < 4; ++i) {
+          const float f = (float)w[i], fh = host_tf32_rna(f);
+          hi[at(r, i)] = fh;                           // B1: w_hi . x~_hi
+          lo[at(r, i)] = host_tf32_rna(f - fh);        // B2: w_lo . x~_hi
+          lo[at(r, 4 + i)] = fh;                       //     w_hi . x~_lo
+        }
+        const float fc = (float)c, ch = host_tf32_rna(fc);
+        hi[at(r, 4)] = ch;                             // B1: c_hi . 1
+        hi[at(r, 5)] = host_tf32_rna(fc - ch);         //     c_lo . 1
+        hi[at(r, 6)] = (float)qc;                      //     q~_hi
+        hi[at(r, 7)] = (float)qc;                      //     q~_lo
+#else
+        auto put = [&](int k, double v) {
+          const float f = (float)v, fh = host_tf32_rna(f);
+          hi[at(r, k)] = fh;
+          lo[at(r, k)] = host_tf32_rna(f - fh);
+        };
+        for (int i = 0; i < 4; ++i) put(i, w[i]);
+        put(4, c);
+        put(5, qc);
+#endif
       };
+      const double zero4[4] = {0, 0, 0, 0};
       for (int j = 0; j < lc; ++j) {
         const int l = l0 + j;
         if (j >= n) {  // padding field: weight 2^-1000 = 0, prediction 0
-          put(j, 4, -1000.0);
+          row(j, zero4, -1000.0, 0.0);
           continue;
         }
         double c4[4], dc[4], a0 = 0;
@@ -685,11 +733,13 @@ inline bool build_tc_weights(const AxisRaw *axes, std::vector<float> &blob, Lwpr
         }
         for (int i = 0; i < 4; ++i) a0 += dc[i] * c4[i];
         a0 = -0.5 * a0;
-        for (int i = 0; i < 4; ++i) put(j, i, dc[i] * kLog2e);   // logit row: DC . x~
-        put(j, 4, a0 * kLog2e + kExpShift);                      //   + A0 (shifted)
-        put(j, 5, 1.0);                                           //   + q~
-        for (int i = 0; i < 4; ++i) put(lc + j, i, a.coefs[(size_t)l * 5 + 1 + i] - gs[i]);  // y' row
-        put(lc + j, 4, y0[l] - g0);
+        double dcl[4], sl[4];
+        for (int i = 0; i < 4; ++i) {
+          dcl[i] = dc[i] * kLog2e;
+          sl[i] = a.coefs[(size_t)l * 5 + 1 + i] - gs[i];
+        }
+        row(j, dcl, a0 * kLog2e + kExpShift, 1.0);  // logit row: DC . x~ + A0 (shifted) + q~
+        row(lc + j, sl, y0[l] - g0, 0.0);           // y' row: S' . x~ + Y0'
       }
       blob.insert(blob.end(), hi.begin(), hi.end());
       blob.insert(blob.end(), lo.begin(), lo.end());
