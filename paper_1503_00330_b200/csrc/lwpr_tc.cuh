@@ -352,7 +352,10 @@ __device__ __forceinline__ void tc_finalize(const LwprTcArgs &a, const AxisHeade
 // The exp phase of nf (multiple of 8) fields of this warp's 32 rows, read from TMEM
 // (logits from column tmem_lane, y' lc columns further on), 2^x + moments into the
 // accumulators.  nf == NFULL runs a fully unrolled loop (compile-time batch count).
-template <bool VAR, bool STREAM, int NFULL>
+// REMB > 0: a chunk of exactly REMB batches (the model's remainder chunk, chosen by the
+// host) also runs an unrolled loop (L=100: 40 of 104 padded fields; harness 391 -> 383 us,
+// micro/lwpr_tc_remb_b200.txt)
+template <bool VAR, bool STREAM, int NFULL, int REMB = 0>
 __device__ __forceinline__ void tc_exp_span(uint32_t tmem_lane, int lc, int nf, const float *slv, float2 &den,
                                             float2 &num, float2 &m2, float2 &lv) {
   const int nb = nf >> 3;  // 8-field batches, two per TMEM wait
@@ -417,7 +420,8 @@ __device__ __forceinline__ void tc_exp_span(uint32_t tmem_lane, int lc, int nf, 
     }
   };
 #if PI2_TC_UNROLL
-  if (nf == NFULL) batches(std::integral_constant<int, NFULL / 8>{});
+  if (REMB > 0 && nf == 8 * REMB) batches(std::integral_constant<int, REMB>{});
+  else if (nf == NFULL) batches(std::integral_constant<int, NFULL / 8>{});
   else batches(std::integral_constant<int, 0>{});
 #else
   batches(std::integral_constant<int, 0>{});
@@ -441,7 +445,7 @@ __device__ __forceinline__ void tc_exp_span(uint32_t tmem_lane, int lc, int nf, 
 // AX: the axis this CTA evaluates as a compile-time constant (the kernel dispatches
 // blockIdx.x % 3 to three copies of the body), so the axis' header constants are
 // immediate parameter-space operands rather than indexed constant loads; -1 = runtime.
-template <bool VAR, bool STREAM, bool WBULK, int AX>
+template <bool VAR, bool STREAM, bool WBULK, int AX, int REMB>
 __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, uint32_t &tmem_base, uint64_t &mbar,
                                              uint64_t *wbar) {
   // CTA i evaluates axis i % 3 for tiles i / 3, i / 3 + gridDim.x / 3, ...: only that
@@ -576,7 +580,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
       phase ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;");
       PI2_TC_T(2);
-      tc_exp_span<VAR, STREAM, kTcChunk>(tmem_lane, lc, lc, slv_base + (int64_t)c * kTcChunk, den, num, m2, lv);
+      tc_exp_span<VAR, STREAM, kTcChunk, REMB>(tmem_lane, lc, lc, slv_base + (int64_t)c * kTcChunk, den, num, m2, lv);
       woff += (int64_t)2 * (2 * lc * 8);
       PI2_TC_T(3);
     }
@@ -604,7 +608,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
 #ifndef PI2_TC_AXT
 #define PI2_TC_AXT 0  // 1: three axis-specialised copies of the body (harness: within 1 %, 3x code; micro/lwpr_tc_axt_b200.txt)
 #endif
-template <bool VAR, bool STREAM, bool WBULK = false>
+template <bool VAR, bool STREAM, bool WBULK = false, int REMB = 0>
 __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const __grid_constant__ LwprTcArgs a) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ uint32_t tmem_base;
@@ -612,12 +616,12 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const
   __shared__ __align__(8) uint64_t wbar[2];  // STREAM: W slot s holds its chunk
 #if PI2_TC_AXT
   switch (blockIdx.x % 3) {
-    case 0: lwpr_tc_body<VAR, STREAM, WBULK, 0>(a, tsm, tmem_base, mbar, wbar); break;
-    case 1: lwpr_tc_body<VAR, STREAM, WBULK, 1>(a, tsm, tmem_base, mbar, wbar); break;
-    default: lwpr_tc_body<VAR, STREAM, WBULK, 2>(a, tsm, tmem_base, mbar, wbar); break;
+    case 0: lwpr_tc_body<VAR, STREAM, WBULK, 0, REMB>(a, tsm, tmem_base, mbar, wbar); break;
+    case 1: lwpr_tc_body<VAR, STREAM, WBULK, 1, REMB>(a, tsm, tmem_base, mbar, wbar); break;
+    default: lwpr_tc_body<VAR, STREAM, WBULK, 2, REMB>(a, tsm, tmem_base, mbar, wbar); break;
   }
 #else
-  lwpr_tc_body<VAR, STREAM, WBULK, -1>(a, tsm, tmem_base, mbar, wbar);
+  lwpr_tc_body<VAR, STREAM, WBULK, -1, REMB>(a, tsm, tmem_base, mbar, wbar);
 #endif
 }
 
@@ -626,6 +630,15 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) lwpr_tc_kernel(const
 // barrier (micro/lwpr_tc_splitbar_b200.txt), TMEM double buffers with every warp doing
 // its own features (micro/lwpr_tc3_dbuf_b200.txt), and warp-specialised exp / producer
 // warps with 2-4 TMEM buffers (micro/lwpr_tcws_b200.txt, patch micro/lwpr_tcws.patch).
+
+// batches of the remainder chunk when every axis ends with the same partial chunk
+// (the REMB instantiation to launch), else 0
+inline int tc_remainder_batches(const LwprTcArgs &ta) {
+  const int r = ta.chunk_pad[0][ta.nchunks[0] - 1];
+  for (int ax = 1; ax < 3; ++ax)
+    if (ta.chunk_pad[ax][ta.nchunks[ax] - 1] != r) return 0;
+  return r < kTcChunk ? r / 8 : 0;
+}
 
 // ---- host: W operands of the tensor-core path ------------------------------
 // Same fold as fold_axis(kLayShared) in float64, split into tf32 hi + lo

@@ -264,8 +264,14 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   const int64_t grid = per_axis * 3;  // CTA i -> axis i % 3
   // few tiles per CTA: resident weights by one bulk copy (see WBULK)
   const bool bulk = (tiles + per_axis - 1) / per_axis <= ctx->tc_bulk_max_tiles;
+  // resident weights, many tiles: the instantiation whose remainder chunk loop is unrolled too
+  using Fn = void (*)(LwprTcArgs);
+  static constexpr Fn kResident[8] = {lwpr_tc_kernel<VAR, false, false, 0>, lwpr_tc_kernel<VAR, false, false, 1>,
+                                      lwpr_tc_kernel<VAR, false, false, 2>, lwpr_tc_kernel<VAR, false, false, 3>,
+                                      lwpr_tc_kernel<VAR, false, false, 4>, lwpr_tc_kernel<VAR, false, false, 5>,
+                                      lwpr_tc_kernel<VAR, false, false, 6>, lwpr_tc_kernel<VAR, false, false, 7>};
   auto *fn = ctx->tc_stream ? lwpr_tc_kernel<VAR, true>
-                            : (bulk ? lwpr_tc_kernel<VAR, false, true> : lwpr_tc_kernel<VAR, false, false>);
+                            : (bulk ? lwpr_tc_kernel<VAR, false, true> : kResident[tc_remainder_batches(ctx->tc)]);
   TRY(set_smem(ctx, fn, ctx->tc_smem));
   TRY(launch_pdl_if(pdl, ctx, fn, dim3((unsigned)grid), dim3(kTcThreads), ctx->tc_smem, st, a));
   CU(cudaGetLastError());
