@@ -80,8 +80,19 @@ int main(int argc, char **argv) {
   // at most kTcCtasPerSm co-resident CTAs (their TMEM allocations must all fit)
   int64_t lvmax = 0;
   for (int i = 0; i < 3; ++i) lvmax = std::max<int64_t>(lvmax, (int64_t)ta.nchunks[i] * kTcChunk);
-  auto *k2 = lwpr_tc_kernel<true, false>;
-  auto *k4 = lwpr_tc_kernel<false, false>;
+  // the product's resident instantiation: remainder chunk unrolled at its batch count
+  using Fn = void (*)(LwprTcArgs);
+  const Fn kv[8] = {lwpr_tc_kernel<true, false, false, 0>, lwpr_tc_kernel<true, false, false, 1>,
+                    lwpr_tc_kernel<true, false, false, 2>, lwpr_tc_kernel<true, false, false, 3>,
+                    lwpr_tc_kernel<true, false, false, 4>, lwpr_tc_kernel<true, false, false, 5>,
+                    lwpr_tc_kernel<true, false, false, 6>, lwpr_tc_kernel<true, false, false, 7>};
+  const Fn km[8] = {lwpr_tc_kernel<false, false, false, 0>, lwpr_tc_kernel<false, false, false, 1>,
+                    lwpr_tc_kernel<false, false, false, 2>, lwpr_tc_kernel<false, false, false, 3>,
+                    lwpr_tc_kernel<false, false, false, 4>, lwpr_tc_kernel<false, false, false, 5>,
+                    lwpr_tc_kernel<false, false, false, 6>, lwpr_tc_kernel<false, false, false, 7>};
+  const int remb = getenv("REMB0") ? 0 : tc_remainder_batches(ta);
+  auto *k2 = kv[remb];
+  auto *k4 = km[remb];
   int smem2 = tc_smem_bytes(wmax, (const void *)k2);
   const bool stream = smem2 < 0 || getenv("STREAM");
   if (stream) {  // W streamed per chunk
