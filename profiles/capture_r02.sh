@@ -11,13 +11,16 @@ for c in C1 C3 C5; do
 done
 python profiles/noise_stream.py > $OUT/noise_stream.json 2>&1 || exit 1
 python profiles/k_sweep.py > $OUT/c5_k_sweep.txt 2>&1 || exit 1
-# launch lists (cold, serialised): the bench command itself, and a C4 step
+# launch lists (cold, serialised): the bench command itself, and C2 / C4 steps (also without the
+# inter-kernel cache flush, for the step's real DRAM traffic)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_bench.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --closed-loop-steps 0 > $OUT/ncu_launch_bench.log 2>&1 || exit 1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file $OUT/launches_c4.csv python profiles/profile_step.py --config C4 --iters 2 > $OUT/ncu_launch_c4.log 2>&1 || exit 1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file $OUT/launches_c2.csv python profiles/profile_step.py --config C2 --iters 2 > $OUT/ncu_launch_c2.log 2>&1 || exit 1
+for c in C2 C4; do
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $OUT/launches_$c.csv python profiles/profile_step.py --config $c --iters 2 > $OUT/ncu_launch_$c.log 2>&1 || exit 1
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none \
+    --csv --log-file $OUT/launches_${c}_nocc.csv python profiles/profile_step.py --config $c --iters 3 > $OUT/ncu_launch_${c}_nocc.log 2>&1 || exit 1
+done
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   -k regex:"attitude|rollout" --log-file $OUT/noise_stream_ncu.csv python profiles/noise_stream.py --reps 1 \
   > $OUT/ncu_noise.log 2>&1 || exit 1
