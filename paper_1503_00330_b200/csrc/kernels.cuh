@@ -526,6 +526,8 @@ struct RollArgs {
   const float *dyn;  // (K, M, N, 3)
   double *costs;     // (K, N)
   uint8_t *crash;    // (K)
+  float *qs;         // horizons past kSmemHorizon: (N, K) stage-cost scratch in global memory (t-major)
+                     // instead of the blocks' shared memory; nullptr otherwise
 };
 
 // opt-in uncertainty penalty (pi2_cost.variance_penalty, an extension; 0 = the
@@ -602,6 +604,9 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   pdl_wait();
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= a.K) return;
+  // this rollout's stage costs: shared memory, or the global scratch for long horizons
+  float *qcol = a.qs ? a.qs + k : sq + threadIdx.x;
+  const int64_t qstride = a.qs ? a.K : (int64_t)blockDim.x;
   const int M = MM > 0 ? MM : a.M;
   const int N = a.N;
   const int S = a.spread ? M : 1;
@@ -730,7 +735,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
         n = 1;
       }
     }
-    sq[t * blockDim.x + threadIdx.x] = (hybrid && a.penalty) ? __fadd_rn(q[0], pen) : q[0];
+    qcol[(int64_t)t * qstride] = (hybrid && a.penalty) ? __fadd_rn(q[0], pen) : q[0];
   }
 
   bool crash = false;
@@ -742,7 +747,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   double acc = 0.0;
   double *out = a.costs + k;  // t-major: S(k, t) at out[t * K]
   for (int t = N - 1; t >= 0; --t) {
-    const double s = __dmul_rn((double)sq[t * blockDim.x + threadIdx.x], dt);
+    const double s = __dmul_rn((double)qcol[(int64_t)t * qstride], dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
     double v = acc;
     if (!isfinite(v)) {
@@ -929,7 +934,10 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
       __syncwarp();
     }
     if (hybrid && a.penalty) qm = __fadd_rn(qm, pen);
-    if (lane_g == 0) sq[t * RPB + grp] = qm;
+    if (lane_g == 0) {
+      if (!a.qs) sq[t * RPB + grp] = qm;
+      else if (live) a.qs[(int64_t)t * a.K + k] = qm;  // long horizon: global scratch
+    }
   }
   // persistent crash of any sub-rollout (controller.py:310)
   bool any = false;
@@ -943,7 +951,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   double acc = 0.0;
   double *out = a.costs + k;  // t-major: S(k, t) at out[t * K]
   for (int t = N - 1; t >= 0; --t) {
-    const double s = __dmul_rn((double)sq[t * RPB + grp], dt);
+    const double s = __dmul_rn((double)(a.qs ? a.qs[(int64_t)t * a.K + k] : sq[t * RPB + grp]), dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
     double v = acc;
     if (!isfinite(v)) {

@@ -56,7 +56,9 @@ struct pi2_ctx {
   bool uva = false;        // pinned host memory is device-accessible (unified addressing)
   bool io_pull = true;     // I/O graph: inputs pulled by io_pull_kernel (PI2_IO_PULL=0: copy node)
   int partials_split = 1;  // partials_split_kernel: 0 never, 1 when few (chunk, t) warps, 2 always
-  int fused = 0;           // device-noise iterations through fused_step_kernel when eligible (PI2_FUSED=1; slower, see DESIGN)
+  int fused = 0;
+  int smem_horizon = kSmemHorizon;  // longer horizons: rollout stage costs in global scratch, no warp-per-rollout
+                                    // kernels (PI2_SMEM_HORIZON lowers it, for tests)           // device-noise iterations through fused_step_kernel when eligible (PI2_FUSED=1; slower, see DESIGN)
   int64_t wide_max_k = kWideMaxK;  // attitude/rollout use a warp per rollout up to this K (PI2_WIDE_MAX_K)
   int64_t tc_bulk_max_tiles = kTcBulkMaxTiles;  // WBULK LWPR up to this many tiles per CTA (PI2_TC_BULK_MAX_TILES)
   LwprTcArgs tc{};
@@ -80,6 +82,8 @@ struct pi2_ctx {
   size_t noise_cap = 0;
   float *d_dynbuf = nullptr;
   size_t dyn_cap = 0;
+  float *d_qs = nullptr;  // long-horizon stage-cost scratch (RollArgs::qs)
+  size_t qs_cap = 0;
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
 
@@ -349,7 +353,7 @@ bool penalty(const pi2_ctx *ctx) {
 template <int MM, bool FAST>
 int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   auto *fn = rollout_kernel<MM, FAST>;
-  const int smem = a.N * kRolloutBlock * (int)sizeof(float);
+  const int smem = a.qs ? 0 : a.N * kRolloutBlock * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + kRolloutBlock - 1) / kRolloutBlock;
   TRY(launch_pdl(ctx, fn, dim3((unsigned)grid), dim3(kRolloutBlock), smem, st, a));
@@ -361,7 +365,7 @@ template <int G, bool FAST>
 int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   auto *fn = rollout_group_kernel<G, FAST>;
   constexpr int RPB = kRolloutBlock / (G > 32 ? 32 : G);
-  const int smem = a.N * RPB * (int)sizeof(float);
+  const int smem = a.qs ? 0 : a.N * RPB * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + RPB - 1) / RPB;
   TRY(launch_pdl(ctx, fn, dim3((unsigned)grid), dim3(kRolloutBlock), smem, st, a));
@@ -389,7 +393,7 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     if (S <= 32) return launch_group_g<32>(ctx, a, fast, st);
     return launch_group_g<64>(ctx, a, fast, st);
   }
-  if (S == 1 && a.K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
+  if (S == 1 && a.K <= ctx->wide_max_k && a.N <= ctx->smem_horizon) {  // latency regime: a warp per rollout
     const unsigned grid = (unsigned)((a.K + kWideWarps - 1) / kWideWarps);
     const int smem = kWideWarps * 11 * a.N * (int)sizeof(float);
     if (hybrid && nav) {
@@ -534,7 +538,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   }
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
   const int psmem = 4 * N * (int)sizeof(double);
-  if (K <= ctx->wide_max_k) {  // latency regime: a warp per rollout
+  if (K <= ctx->wide_max_k && N <= ctx->smem_horizon) {  // latency regime: a warp per rollout
     const unsigned wgrid = (unsigned)((K + kWideWarps - 1) / kWideWarps);
     const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
     if (noise_dev) {
@@ -587,6 +591,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   a.dyn = dyn_dev;
   a.costs = costs;
   a.crash = crash;
+  if (N > ctx->smem_horizon) a.qs = ctx->d_qs;  // long horizon: stage costs through the (N, K) global scratch
   return launch_rollout(ctx, a, st);
 }
 
@@ -698,7 +703,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
     return fail(nullptr, PI2_ERR_INVALID, "num_rollouts, sub_rollouts, horizon_steps must be >= 1");
   if (dims->sub_rollouts > PI2_MAX_SUB_ROLLOUTS)
     return fail(nullptr, PI2_ERR_INVALID, "sub_rollouts must be <= %d", PI2_MAX_SUB_ROLLOUTS);
-  if (dims->horizon_steps > 400) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= 400");
+  if (dims->horizon_steps > kMaxHorizon) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= %d", kMaxHorizon);
   if (dims->rollout_offset < 0) return fail(nullptr, PI2_ERR_INVALID, "rollout_offset must be >= 0");
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -726,6 +731,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if (const char *e = getenv("PI2_WIDE_MAX_K")) ctx->wide_max_k = std::atoll(e);
   if (const char *e = getenv("PI2_TC_BULK_MAX_TILES")) ctx->tc_bulk_max_tiles = std::atoll(e);
   if (const char *e = getenv("PI2_FUSED")) ctx->fused = std::atoi(e);
+  if (const char *e = getenv("PI2_SMEM_HORIZON")) ctx->smem_horizon = std::min(std::atoi(e), kSmemHorizon);
   {
     int uva = 0;
     cudaDeviceGetAttribute(&uva, cudaDevAttrUnifiedAddressing, device);
@@ -750,6 +756,10 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   ALLOC(ctx->d_xin, sizeof(float4) * K * N);
   ALLOC(ctx->d_ang_last, sizeof(float4) * K);
   ALLOC(ctx->d_lw, sizeof(float4) * K * N * 2);
+  if (N > ctx->smem_horizon) {  // long horizons: the rollout kernels' stage costs go through global memory
+    ALLOC(ctx->d_qs, sizeof(float) * K * N);
+    ctx->qs_cap = sizeof(float) * K * N;
+  }
   ALLOC(ctx->d_costs, sizeof(double) * K * N);
   ALLOC(ctx->d_crash, K);
   ALLOC(ctx->d_partials, sizeof(double) * PI2_PARTIAL_WIDTH * ctx->n_chunks * N);
@@ -780,7 +790,7 @@ void pi2_destroy(pi2_ctx *ctx) {
   invalidate_graph(ctx);
   void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_io,     ctx->d_plan2,    ctx->d_xin,
                   ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
-                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch, ctx->d_z};
+                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch, ctx->d_z, ctx->d_qs};
   for (void *p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_io) cudaFreeHost(ctx->h_io);
