@@ -431,6 +431,27 @@ class Rig:
             clocks.mark_end()
         return self.max_over_ranks(start.elapsed_time(end)) / steps
 
+    def time_device_iterations(self, iterations, steps, warmup):
+        """ms per control step with `iterations` optimisation iterations per step (N=1: the
+        reference's default is 2); one CUDA graph per step, CUDA events."""
+        import torch
+
+        from paper_1503_00330_b200.controller import optimize_args
+
+        cfg = self.P.PiConfig(num_rollouts=self.cfg.num_rollouts, sub_rollouts=self.cfg.sub_rollouts,
+                              horizon_steps=self.cfg.horizon_steps, iterations_per_step=iterations, rng_seed=0)
+        for w in range(warmup):
+            self.ctx.call("pi2_iterate_device", optimize_args(cfg, 20_000 + w, use_graph=True), self.sptr)
+        self.barrier()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(self.stream)
+        for s in range(steps):
+            self.ctx.call("pi2_iterate_device", optimize_args(cfg, s, use_graph=True), self.sptr)
+        end.record(self.stream)
+        end.synchronize()
+        self.barrier()
+        return start.elapsed_time(end) / steps
+
     def time_api(self, steps, warmup):
         """(total seconds, per-step latencies in ms) of the public-API step, max over ranks."""
         for w in range(warmup):
@@ -593,6 +614,14 @@ def run_ours(args, rank: int, world: int, local: int):
     kern, share = _abi.C.c_int32(), _abi.C.c_double()
     rig.ctx.call("pi2_lwpr_kernel", int(M > 1), _abi.C.byref(kern), _abi.C.byref(share))
 
+    # ---- the reference's default of 2 iterations per control step (N=1)
+    it2 = None
+    if world == 1:
+        it2_ms = rig.time_device_iterations(2, max(5, args.steps // 4), args.warmup)
+        it2 = {"iterations_per_step": 2, "ms_per_step": it2_ms, "value": 2 * K * T / (it2_ms * 1e-3), "unit": UNIT,
+               "what": "the same workload with the reference's default iterations_per_step=2 (PiConfig, "
+                       "controller.py:79): device ms per control step, rollout-steps of both iterations per second"}
+
     # ---- end to end through the public API (host state/plan in, control/plan out)
     e2e_s, lat = rig.time_api(args.steps, args.warmup)
 
@@ -684,6 +713,8 @@ def run_ours(args, rank: int, world: int, local: int):
         line["noise_stream"] = ns
     if ns_obj is not None:
         line["north_star"] = ns_obj
+    if it2 is not None:
+        line["iterations_per_step_2"] = it2
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(cfgd, min(args.cpu_sample, K), min_seconds=args.cpu_seconds)
         cb.pop("step_times_s", None)
