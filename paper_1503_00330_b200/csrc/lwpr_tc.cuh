@@ -121,6 +121,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// The same MMA issued by a converged warp: every lane executes the instruction and
+// elect.sync picks one inside the asm, so the descriptors stay in uniform registers.
+// Issued from a divergent `tid == 0` branch, ptxas wraps every UTCHMMA in an ELECT /
+// BRA.U.ANY waterfall (profiles/micro/mma_tmem_a_b200.txt: 2 MMAs + commit issue in
+// ~100 clocks converged vs ~260 from the divergent branch).
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t mbar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(mbar)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
@@ -216,6 +235,9 @@ __device__ __forceinline__ void tc_trace(int slot, int &n, int i) {
 // 3xTF32 as TWO MMAs per chunk instead of three: the same product terms hi.hi + hi.lo +
 // lo.hi rearranged along K (A1 = [x~hi, 1, 1, q~hi, q~lo] . B1 = [Whi, A0hi, A0lo, 1, 1] and
 // A2 = [x~hi, x~lo] . B2 = [Wlo, Whi]); operands keep their sizes
+#ifndef PI2_TC_ELECT  // chunk MMAs issued by converged warp 0 with elect.sync (else thread 0)
+#define PI2_TC_ELECT 0  // 1 measured slower in situ: L=100 385 -> 400 us, L=200 677 -> 698 (micro/tc_elect_b200.txt)
+#endif
 #ifndef PI2_TC_PACK2
 #define PI2_TC_PACK2 1
 #endif
@@ -547,6 +569,27 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();  // A written, TMEM free
       PI2_TC_T(1);
+#if PI2_TC_ELECT
+      if (warp == 0) {  // converged: one elected lane issues (uniform descriptors)
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
+        const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);
+        if (STREAM) mbar_wait(wbar_addr + 8 * (nw & 1), (nw >> 1) & 1);  // this chunk's W landed
+        const uint32_t wb = STREAM ? sw_addr + (nw & 1) * (uint32_t)(kTcWSlotFloats * 4) : sw_addr + (uint32_t)(woff * 4);
+        const uint64_t b_hi = umma_smem_desc(wb), b_lo = umma_smem_desc(wb + (uint32_t)(2 * lc * 8 * 4));
+#if PI2_TC_PACK2
+        mma_tf32_elect(tmem, a_hi, b_hi, idesc, 0);  // A1 . B1
+        mma_tf32_elect(tmem, a_lo, b_lo, idesc, 1);  // A2 . B2
+#else
+        mma_tf32_elect(tmem, a_hi, b_hi, idesc, 0);
+        mma_tf32_elect(tmem, a_hi, b_lo, idesc, 1);
+        mma_tf32_elect(tmem, a_lo, b_hi, idesc, 1);
+#endif
+        mma_commit_elect(mbar_addr);
+        // the other slot held chunk nw - 1, whose MMA completed before this chunk's barrier
+        if (STREAM && tid == 0 && (c + 1 < nch || tile + tstride < ntiles)) load_w(c + 1 < nch ? c + 1 : 0, (nw + 1) & 1);
+      }
+#else
       if (tid == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
@@ -567,6 +610,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
         // the other slot held chunk nw - 1, whose MMA completed before this chunk's barrier
         if (STREAM && (c + 1 < nch || tile + tstride < ntiles)) load_w(c + 1 < nch ? c + 1 : 0, (nw + 1) & 1);
       }
+#endif
       if (c == 0) {  // in the MMA's shadow: finish tile t - 1, stage tile t + 1
         tc_finalize<VAR>(a, h, ax, row_prev, xt_prev, q_prev, dn_p, nm_p, m2_p, lv_p);
         if (tile + tstride < ntiles) {
