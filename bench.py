@@ -74,6 +74,8 @@ def parse():
                    help="--impl reference: wall-clock budget of the timed steps (full K each)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-north-star", action="store_true")
+    p.add_argument("--no-other-configs", action="store_true",
+                   help="N=1: skip the short measurements of the other BASELINE configs (C1, C3, C5 + K sweep)")
     p.add_argument("--closed-loop-steps", type=int, default=500,
                    help="north star: control steps of the closed-loop trial (BASELINE C4: 500); 0 disables")
     return p.parse_args()
@@ -574,6 +576,50 @@ def north_star(args, world, local, stream, dist, rank):
     return out
 
 
+def lwpr_frac(rig, cfgd):
+    """Stage ms of one iteration (CUDA events, pi2_profile_iteration) and the LWPR kernel's
+    algorithmic 2^x rate against the MUFU peak, as in the headline roofline."""
+    from paper_1503_00330_b200.controller import optimize_args
+
+    _abi = rig._abi
+    stage_ms = (_abi.C.c_double * 5)()
+    rig.ctx.call("pi2_profile_iteration", optimize_args(rig.cfg, 0, use_graph=False), 5, stage_ms)
+    stages = dict(zip(["attitude", "lwpr", "rollout_cost", "partials", "combine"], list(stage_ms)))
+    exps = cfgd["K"] * cfgd["T"] * 3 * cfgd["L"]
+    mufu_peak = float(measured_peaks().get("mufu_ex2_per_s", 4.60e12))
+    return stages, exps / (stages["lwpr"] / 1e3) / mufu_peak
+
+
+def other_configs(args, local, stream):
+    """N=1: the other BASELINE configs measured briefly in the same run (device ms per step
+    over back-to-back graph replays, e2e p50/p99 through receding_horizon_step, the LWPR
+    kernel's MUFU fraction), and C5's rollout-count sweep K = 2^10 .. 2^22."""
+    import torch
+
+    out = {}
+    for name, steps in (("C1", 50), ("C3", 10), ("C5", 10)):
+        cfgd, desc = workload(name, 1, "strong")
+        rig = Rig(cfgd, 1, local, stream, None)
+        ms = rig.time_device(steps, 3)
+        _, lat = rig.time_api(min(steps, 10), 2)
+        stages, frac = lwpr_frac(rig, cfgd)
+        out[name] = {"workload": desc, "device_ms_per_step": ms, "value": cfgd["K"] * cfgd["T"] / (ms * 1e-3),
+                     "unit": UNIT, "e2e_ms": lat, "stages_ms": stages, "lwpr_mufu_frac": frac, "steps": steps}
+        del rig
+        torch.cuda.empty_cache()
+    sweep = []
+    for lk in range(10, 23, 2):
+        cfgd, _ = workload("C5", 1, "strong")
+        cfgd["K"] = 1 << lk
+        rig = Rig(cfgd, 1, local, stream, None)
+        ms = rig.time_device(10 if lk >= 18 else 50, 3)
+        sweep.append({"K": cfgd["K"], "device_ms_per_step": ms, "value": cfgd["K"] * cfgd["T"] / (ms * 1e-3)})
+        del rig
+        torch.cuda.empty_cache()
+    out["C5_k_sweep"] = {"T": 50, "L": 200, "M": 1, "unit": UNIT, "points": sweep}
+    return out
+
+
 def run_ours(args, rank: int, world: int, local: int):
     import torch
 
@@ -634,6 +680,8 @@ def run_ours(args, rank: int, world: int, local: int):
     ns_obj = None
     if not args.no_north_star:
         ns_obj = north_star(args, world, local, stream, dist, rank)
+    oc = (other_configs(args, local, stream)
+          if world == 1 and args.config == "C2" and not args.no_other_configs else None)
 
     if rank != 0:
         return None
@@ -715,6 +763,8 @@ def run_ours(args, rank: int, world: int, local: int):
         line["north_star"] = ns_obj
     if it2 is not None:
         line["iterations_per_step_2"] = it2
+    if oc is not None:
+        line["other_configs"] = oc
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(cfgd, min(args.cpu_sample, K), min_seconds=args.cpu_seconds)
         cb.pop("step_times_s", None)
