@@ -348,7 +348,7 @@ class Rig:
         import paper_1503_00330_b200 as P
         from paper_1503_00330_b200 import _abi, synthetic
         from paper_1503_00330_b200.controller import dynamics_struct
-        from paper_1503_00330_b200.simworld import cost_struct
+        from paper_1503_00330_b200.simworld import apply_cost
 
         self.P, self._abi = P, _abi
         self.cfgd, self.world, self.local, self.stream, self.dist = cfgd, world, local, stream, dist
@@ -373,7 +373,7 @@ class Rig:
             self.ctx = self.eng.context(K, T)
             self.k_local = K
             self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, self.plan0.lo, self.plan0.hi))
-            self.ctx.call("pi2_set_cost", cost_struct(self.cost))
+            apply_cost(self.ctx, self.cost)
             self.ctx.call("pi2_load_plan", _abi.ptr(self.state.as_array()),
                           _abi.ptr(np.ascontiguousarray(self.plan0.controls)), self.sptr)
 

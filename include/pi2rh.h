@@ -137,6 +137,11 @@ int pi2_set_lwpr_axis(pi2_ctx *ctx, int32_t axis, int32_t num_fields, int32_t in
 int pi2_select_model(pi2_ctx *ctx, int32_t kind, double param);
 /* RolloutCost / ThresholdCost; simworld.py:141-146. */
 int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *cost);
+/* The navigation cost's full obstacle list, any length (RolloutCost.obstacles,
+ * simworld.py:141-146, has no limit; pi2_cost holds PI2_MAX_OBSTACLES): (n, 2)
+ * float32 (x, y), summed in list order like simworld.py:188-190.  Call after
+ * pi2_set_cost (which resets the list to the struct's). */
+int pi2_set_cost_obstacles(pi2_ctx *ctx, int32_t n, const float *obstacles_xy);
 
 /* ---- hot path ----------------------------------------------------------- */
 /* RolloutEngine.evaluate (controller.py:197-247): perturb + clip, FP64

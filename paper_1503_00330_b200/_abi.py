@@ -61,6 +61,7 @@ _SIGNATURES = {
     "pi2_set_lwpr_axis": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P]),
     "pi2_select_model": (C.c_int, [_P, C.c_int32, C.c_double]),
     "pi2_set_cost": (C.c_int, [_P, C.POINTER(Cost)]),
+    "pi2_set_cost_obstacles": (C.c_int, [_P, C.c_int32, _P]),
     "pi2_evaluate": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, _P, _P]),
     "pi2_evaluate_device": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, _P, _P, _P]),
     "pi2_evaluate_device_noise": (C.c_int, [_P, _P, _P, C.POINTER(OptimizeArgs), C.c_int32, _P, _P, _P]),

@@ -27,7 +27,7 @@ import numpy as np
 from . import _abi, rng
 from .dynamics import AnalyticModel, Control, QuadParams, QuadState
 from .lwpr import stage_axis
-from .simworld import cost_struct
+from .simworld import apply_cost
 
 NOISE_MODES = ("reference", "device")
 
@@ -226,7 +226,7 @@ class RolloutEngine:
             return
         self._bound.pop(id(ctx), None)
         ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
-        ctx.call("pi2_set_cost", cost_struct(cost_model))
+        apply_cost(ctx, cost_model)
         self._bound[id(ctx)] = key
 
     def evaluate(self, state: QuadState, plan: ControlPlan, noise, cost_model,

@@ -70,6 +70,9 @@ struct StepArgs {
   double neg_inv_temp;  // -1 / temperature (controller.py:368)
   double ceiling;       // cost_ceiling (controller.py:243-246)
   pi2_cost cost;
+  // obstacles PI2_MAX_OBSTACLES .. cost.n_obstacles - 1 as (x, y) pairs in HBM (the
+  // reference takes any count, simworld.py:141-146); nullptr when the struct holds them all
+  const float *extra_obstacles;
 };
 
 struct DynParams {

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) fused_step_kernel(co
   pdl_wait();
   const StepArgs *sa_args = f.sa;
   if (tid == 0) cost = sa_args->cost;
+  const float *xobs = nullptr;  // the host takes this kernel only while pi2_cost holds every obstacle
   const DynParams &dp = f.dp;
   const int S = f.spread ? f.M : 1;
   const Key128 ck = iter_key(sa_args->key_prefix[0], (uint64_t)f.iteration);
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) fused_step_kernel(co
         bool cm = ((crashed >> m) & 1u) != 0;
         cm = cm | nav_crash_now(cost, pos[0], pos[1], pos[2]);
         crashed |= (cm ? 1u : 0u) << m;
-        q[m] = nav_stage_cost(cost, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, cm);
+        q[m] = nav_stage_cost<false>(cost, xobs, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, cm);
       }
       int n = S;  // pairwise halving while even, plain mean when odd (controller.py:314-319)
       while (n > 1) {

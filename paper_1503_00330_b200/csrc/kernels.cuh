@@ -564,7 +564,12 @@ __device__ __forceinline__ float obstacle_term(float px, float py, float ox, flo
 }
 
 // stage cost q(x) in the reference's float32 operation order (simworld.py:166-198)
-__device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, float py, float pz,
+// extra: obstacles PI2_MAX_OBSTACLES.. (StepArgs::extra_obstacles), summed in the same order.
+// XOBS = false (the FAST kernels, which the host runs only while the struct holds the whole
+// list) drops that loop: it cost the group kernel 7 us at C2 even when never entered.
+template <bool XOBS = true>
+__device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, const float *__restrict__ extra, float px, float py,
+                                                float pz,
                                                 float vx, float vy, float vz, float angterm,
                                                 bool crashed) {
   float d = __fsub_rn(px, c.waypoint[0]);
@@ -581,8 +586,13 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, float px, flo
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (i < c.n_obstacles) out = __fadd_rn(out, obstacle_term(px, py, c.obstacles[2 * i], c.obstacles[2 * i + 1]));
-  for (int i = 4; i < c.n_obstacles; ++i)
+  const int n_struct = c.n_obstacles < PI2_MAX_OBSTACLES ? c.n_obstacles : PI2_MAX_OBSTACLES;
+  for (int i = 4; i < n_struct; ++i)
     out = __fadd_rn(out, obstacle_term(px, py, c.obstacles[2 * i], c.obstacles[2 * i + 1]));
+  if (XOBS)
+    for (int i = PI2_MAX_OBSTACLES; i < c.n_obstacles; ++i)
+      out = __fadd_rn(out, obstacle_term(px, py, __ldg(extra + 2 * (i - PI2_MAX_OBSTACLES)),
+                                         __ldg(extra + 2 * (i - PI2_MAX_OBSTACLES) + 1)));
   return __fadd_rn(out, crashed ? 10.0f : 0.0f);
 }
 
@@ -621,6 +631,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
   const pi2_cost &nav = cost;
+  const float *xobs = a.sa->extra_obstacles;  // obstacles past the struct's PI2_MAX_OBSTACLES
 
   float cs[MCAP][3], ccs[MCAP][3];
   bool crashed[MCAP];
@@ -714,7 +725,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
         q[m] = pos[2] > cost.threshold ? 1.0f : 0.0f;
       } else {
         crashed[m] = crashed[m] | nav_crash_now(nav, pos[0], pos[1], pos[2]);  // no short-circuit branch
-        q[m] = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[m]);
+        q[m] = nav_stage_cost<!FAST>(nav, xobs, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[m]);
       }
     }
     // sub-rollout mean: pairwise halving while even, plain mean when odd
@@ -805,6 +816,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   const uint64_t kg = (uint64_t)(a.k_off + k);
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const pi2_cost &nav = cost;
+  const float *xobs = a.sa->extra_obstacles;  // obstacles past the struct's PI2_MAX_OBSTACLES
   const int64_t kk = live ? k : 0;
   const bool device_dyn = FAST || a.device_dyn;
   const bool two_point = !FAST && a.model == PI2_MODEL_TWO_POINT;
@@ -892,7 +904,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
           q[j] = pos[2] > cost.threshold ? 1.0f : 0.0f;
         } else {
           crashed[j] = crashed[j] | nav_crash_now(nav, pos[0], pos[1], pos[2]);  // no short-circuit branch
-          q[j] = nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[j]);
+          q[j] = nav_stage_cost<!FAST>(nav, xobs, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angterm, crashed[j]);
         }
       }
     }
@@ -1042,6 +1054,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
   const int model = FAST ? PI2_MODEL_HYBRID_LWPR : a.model;
   const bool threshold_cost = !FAST && cost.kind == PI2_COST_THRESHOLD;
   const pi2_cost &nav = cost;
+  const float *xobs = a.sa->extra_obstacles;  // obstacles past the struct's PI2_MAX_OBSTACLES
   for (int t = lane; t < N; t += 32) {
     const int64_t row = (int64_t)t * a.K + k;
     float mn[3];
@@ -1103,7 +1116,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) rollout_wide_kernel(RollArgs 
     carry = carry || b != 0;
     if (t < N) {
       q[t] = threshold_cost ? (pos[2] > cost.threshold ? 1.0f : 0.0f)
-                            : nav_stage_cost(nav, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
+                            : nav_stage_cost<!FAST>(nav, xobs, pos[0], pos[1], pos[2], vel[0], vel[1], vel[2], angt[t], crashed);
       if (model == PI2_MODEL_HYBRID_LWPR && a.penalty)
         q[t] = __fadd_rn(q[t], variance_term(cost.variance_penalty, ld_planes(a.lw_std, a.lw_plane, (int64_t)t * a.K + k)));
     }

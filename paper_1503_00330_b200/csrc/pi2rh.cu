@@ -82,6 +82,9 @@ struct pi2_ctx {
   size_t noise_cap = 0;
   float *d_dynbuf = nullptr;
   size_t dyn_cap = 0;
+  float *d_xobs = nullptr;  // navigation-cost obstacles past PI2_MAX_OBSTACLES (StepArgs::extra_obstacles)
+  size_t xobs_cap = 0;
+  std::vector<float> h_xobs;  // their host copy (re-staged only on change)
   float *d_qs = nullptr;  // long-horizon stage-cost scratch (RollArgs::qs)
   size_t qs_cap = 0;
   void *d_scratch = nullptr;
@@ -378,9 +381,13 @@ int launch_group_g(pi2_ctx *ctx, const RollArgs &a, bool fast, cudaStream_t st) 
   return fast ? launch_group_t<G, true>(ctx, a, st) : launch_group_t<G, false>(ctx, a, st);
 }
 
+// the whole obstacle list sits in pi2_cost (no StepArgs::extra_obstacles): the FAST
+// rollout kernels and the fused kernel, which have no loop over the HBM tail, may run
+inline bool struct_obstacles(const pi2_ctx *ctx) { return ctx->cost.n_obstacles <= PI2_MAX_OBSTACLES; }
+
 int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const int S = a.spread ? a.M : 1;
-  const bool nav = ctx->cost.kind == PI2_COST_NAVIGATION;
+  const bool nav = ctx->cost.kind == PI2_COST_NAVIGATION && struct_obstacles(ctx);  // FAST-eligible
   const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
   // sub-rollouts on lanes (any model but the analytic one, which is never spread);
   // 33..64 on 32 lanes with two each (S <= PI2_MAX_SUB_ROLLOUTS = 64)
@@ -426,6 +433,7 @@ void fill_args(pi2_ctx *ctx, const double *state, const pi2_optimize_args *opt, 
   StepArgs &h = *ctx->h_args;
   if (state) std::memcpy(h.state, state, sizeof h.state);
   h.cost = ctx->cost;
+  h.extra_obstacles = ctx->cost.n_obstacles > PI2_MAX_OBSTACLES ? ctx->d_xobs : nullptr;
   h.ceiling = ceiling;
   if (opt) {
     h.neg_inv_temp = -1.0 / opt->temperature;
@@ -459,7 +467,9 @@ int stage_plan(pi2_ctx *ctx, const double *plan, cudaStream_t st) {
 // sub-rollouts fit (S <= kFusedMaxM); its shared memory must leave room for
 // kTcCtasPerSm CTAs.  Returns the sub-rollout template (1, 2, 4) or 0.
 int fused_mm(pi2_ctx *ctx) {
-  if (!ctx->fused || ctx->model != PI2_MODEL_HYBRID_LWPR || ctx->cost.kind != PI2_COST_NAVIGATION) return 0;
+  if (!ctx->fused || ctx->model != PI2_MODEL_HYBRID_LWPR || ctx->cost.kind != PI2_COST_NAVIGATION ||
+      !struct_obstacles(ctx))
+    return 0;
   if (ensure_params(ctx) != PI2_OK || !ctx->tc_ok || ctx->K <= ctx->wide_max_k) return 0;
   const bool var = spread(ctx) || penalty(ctx);
   if (!tc_wanted(ctx, var)) return 0;
@@ -790,7 +800,8 @@ void pi2_destroy(pi2_ctx *ctx) {
   invalidate_graph(ctx);
   void *bufs[] = {ctx->d_params, ctx->d_tc, ctx->d_io,     ctx->d_plan2,    ctx->d_xin,
                   ctx->d_ang_last, ctx->d_lw,   ctx->d_costs, ctx->d_crash,    ctx->d_partials,
-                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch, ctx->d_z, ctx->d_qs};
+                  ctx->d_root,   ctx->d_noise,  ctx->d_dynbuf, ctx->d_scratch, ctx->d_z, ctx->d_qs,
+                  ctx->d_xobs};
   for (void *p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_io) cudaFreeHost(ctx->h_io);
@@ -874,14 +885,47 @@ int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *c) {
   if (c->kind != PI2_COST_NAVIGATION && c->kind != PI2_COST_THRESHOLD)
     return fail(ctx, PI2_ERR_UNSUPPORTED, "unknown cost kind %d", c->kind);
   if (c->n_obstacles < 0 || c->n_obstacles > PI2_MAX_OBSTACLES)
-    return fail(ctx, PI2_ERR_UNSUPPORTED, "at most %d obstacles", PI2_MAX_OBSTACLES);
+    return fail(ctx, PI2_ERR_UNSUPPORTED, "at most %d obstacles in pi2_cost (longer lists: pi2_set_cost_obstacles)",
+                PI2_MAX_OBSTACLES);
   if (!(c->variance_penalty >= 0.0f) || !std::isfinite(c->variance_penalty))
     return fail(ctx, PI2_ERR_INVALID, "variance_penalty must be finite and >= 0");
   // kernel variants depend on the kind and on whether the penalty is on
-  if (ctx->have_cost && (ctx->cost.kind != c->kind || (ctx->cost.variance_penalty > 0) != (c->variance_penalty > 0)))
+  if (ctx->have_cost && (ctx->cost.kind != c->kind || (ctx->cost.variance_penalty > 0) != (c->variance_penalty > 0) ||
+                         !struct_obstacles(ctx)))
     invalidate_graph(ctx);
   ctx->cost = *c;
   ctx->have_cost = true;
+  return PI2_OK;
+}
+
+int pi2_set_cost_obstacles(pi2_ctx *ctx, int32_t n, const float *xy) {
+  if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
+  if (!ctx->have_cost || ctx->cost.kind != PI2_COST_NAVIGATION)
+    return fail(ctx, PI2_ERR_STATE, "set a navigation cost (pi2_set_cost) first");
+  if (n < 0 || (n > 0 && !xy)) return fail(ctx, PI2_ERR_INVALID, "bad obstacle list");
+  const int head = n < PI2_MAX_OBSTACLES ? n : PI2_MAX_OBSTACLES;
+  // kernel selection depends on whether the list fits the struct (struct_obstacles)
+  if ((ctx->cost.n_obstacles > PI2_MAX_OBSTACLES) != (n > PI2_MAX_OBSTACLES)) invalidate_graph(ctx);
+  std::memset(ctx->cost.obstacles, 0, sizeof ctx->cost.obstacles);
+  std::memcpy(ctx->cost.obstacles, xy, sizeof(float) * 2 * head);
+  ctx->cost.n_obstacles = n;
+  std::vector<float> tail(xy + 2 * head, xy + 2 * (size_t)n);
+  if (tail == ctx->h_xobs) return PI2_OK;
+  // rare (the list changed): no kernel of this device may still read the old list
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaDeviceSynchronize());
+  if (tail.size() > ctx->xobs_cap) {
+    if (ctx->d_xobs) CU(cudaFree(ctx->d_xobs));
+    ctx->d_xobs = nullptr;
+    ctx->xobs_cap = 0;
+    if (cudaMalloc(&ctx->d_xobs, tail.size() * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, PI2_ERR_OOM, "obstacle list allocation failed");
+    }
+    ctx->xobs_cap = tail.size();
+  }
+  if (!tail.empty()) CU(cudaMemcpy(ctx->d_xobs, tail.data(), tail.size() * sizeof(float), cudaMemcpyHostToDevice));
+  ctx->h_xobs = std::move(tail);
   return PI2_OK;
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 from . import _abi
 from .controller import ControlPlan, PiConfig, _cost_key, dynamics_struct, model_kind, optimize_args
 from .lwpr import stage_axis
-from .simworld import cost_struct
+from .simworld import apply_cost
 
 
 def shard_range(num_rollouts: int, rank: int, world: int, chunk: int | None = None) -> tuple[int, int]:
@@ -124,7 +124,7 @@ class ShardedEngine:
         if key == self._bound and key[-1] is not None:
             return
         self.ctx.call("pi2_set_dynamics", dynamics_struct(self.params, plan.lo, plan.hi))
-        self.ctx.call("pi2_set_cost", cost_struct(cost_model))
+        apply_cost(self.ctx, cost_model)
         self._bound = key
 
     def _enqueue_step(self, iterations: int, temperature: float, stream) -> None:

@@ -118,6 +118,37 @@ def test_evaluate_matches_oracle(K, N, L, M, full):
     assert np.all(du_err(new.controls, RO.update(plan.controls, lo, hi, rc, noise, 1.0), plan.controls) < DU_TOL)
 
 
+@pytest.mark.parametrize("K,M", [(600, 1), (9000, 1), (3000, 4), (1500, 3)])
+def test_many_obstacles_match_oracle(K, M):
+    """Obstacle lists longer than pi2_cost holds (the reference has no limit,
+    simworld.py:141-146, :188-190): the first PI2_MAX_OBSTACLES ride in the struct, the
+    rest in HBM (pi2_set_cost_obstacles), summed in list order.  Covers the warp-,
+    thread- and group-per-rollout kernels, a changed list on the same engine (re-staged),
+    and a short list afterwards (reset)."""
+    N, L = 40, 24
+    stacks = synthetic.hybrid_stacks(L, seed=K + M)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=K)
+    base = P.Task.default()
+    state = P.QuadState.hover(base.spawn + np.array([0.05, -0.1, 0.07]))
+    plan = P.ControlPlan.hover(params, N)
+    noise = P.sample_noise(cfg, 1, 0)
+    dyn = P.sample_dynamics_noise(cfg, 1, 0) if M > 1 else None
+    eng = P.RolloutEngine(model, cfg, device=0)
+    om = RO.Model(stacks)
+    lo, hi = om.dyn.bounds()
+    rng = np.random.default_rng(K)
+    for n_obs in (40, 23, 3):
+        # obstacles around the spawn so that their terms matter to the costs
+        obs = base.spawn[:2] + rng.uniform(-0.6, 0.6, size=(n_obs, 2))
+        task = P.Task(base.waypoints, obs)
+        b = eng.evaluate(state, plan, noise, P.RolloutCost(task, 1), dyn)
+        rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise, RO.Cost(task.waypoints[1], obs), dyn, M)
+        np.testing.assert_array_equal(b.crash_flags, rf)
+        assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL, n_obs
+
+
 def test_frozen_lwpr_predict_matches_reference():
     z = load("lwpr")
     st = stacks_from(z, "diag_")

@@ -72,6 +72,13 @@ def test_plugin_classification():
     assert list(c.waypoint) == [0.0, pytest.approx(1.1), 1.0]
     with pytest.raises(TypeError):
         cost_struct(object())
+    # longer obstacle lists than the struct holds: the struct carries the first
+    # MAX_OBSTACLES and apply_cost stages the whole list (pi2_set_cost_obstacles)
+    rng = np.random.default_rng(0)
+    task = P.Task(P.Task.default().waypoints, rng.uniform(-1.5, 1.5, size=(40, 2)))
+    c = cost_struct(P.RolloutCost(task, 0))
+    assert c.n_obstacles == _abi.MAX_OBSTACLES
+    assert list(c.obstacles)[:2] == [pytest.approx(float(np.float32(v))) for v in task.obstacles[0]]
 
 
 def test_lwpr_model_reference_constructor():
