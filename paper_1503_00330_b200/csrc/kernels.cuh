@@ -1157,6 +1157,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+#ifndef PI2_PARTIALS_ZAHEAD
+#define PI2_PARTIALS_ZAHEAD 2  // stored-normal loads issued this many elements ahead (0: in the loop);
+                               // C2 partials 32 -> 26 us, C4 379 -> 285 us; 4 (70 regs) 28 / 330 us (micro/partials_zahead_b200.txt)
+#endif
 __global__ void __launch_bounds__(32 * kChunkWarps)
     partials_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
                     const double *__restrict__ eps, const float4 *zin, const StepArgs *__restrict__ sa, int iteration,
@@ -1178,6 +1182,33 @@ __global__ void __launch_bounds__(32 * kChunkWarps)
   m = warp_min(m);
   double z = 0.0, v[4] = {0.0, 0.0, 0.0, 0.0};
   const Key128 ck = (eps || zin) ? Key128{0, 0} : iter_key(sa->key_prefix[0], (uint64_t)iteration);
+#if PI2_PARTIALS_ZAHEAD > 0
+  if (zin && !eps) {  // stored normals: PI2_PARTIALS_ZAHEAD element loads in flight ahead of the f64 exp chain
+    constexpr int ZA = PI2_PARTIALS_ZAHEAD;
+    float4 zb[ZA];
+#pragma unroll
+    for (int j = 0; j < ZA; ++j) {
+      const int64_t k = k0 + lane + 32 * j;
+      zb[j] = k < K ? __ldcg(zin + (int64_t)t * K + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const float4 zc = zb[j % ZA];
+      if (j + ZA < J) {
+        const int64_t kn = k0 + lane + 32 * (j + ZA);
+        zb[j % ZA] = kn < K ? __ldcg(zin + (int64_t)t * K + kn) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const int64_t k = k0 + lane + 32 * j;
+      if (k >= K) continue;
+      const double w = exp(__dmul_rn(__dsub_rn(s[j], m), neg_inv));
+      double e[4];
+      eps_from_z(sa, zc, e);
+      z = __dadd_rn(z, w);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = __dadd_rn(v[c], __dmul_rn(w, e[c]));
+    }
+  } else
+#endif
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int64_t k = k0 + lane + 32 * j;
