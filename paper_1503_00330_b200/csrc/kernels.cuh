@@ -596,6 +596,10 @@ __device__ __forceinline__ float nav_stage_cost(const pi2_cost &c, const float *
   return __fadd_rn(out, crashed ? 10.0f : 0.0f);
 }
 
+#ifndef PI2_ROLL1_AHEAD
+#define PI2_ROLL1_AHEAD 1  // rows in flight ahead of the step using them in rollout_kernel; 2 (64 regs) was
+                           // slower: C4 rollout 395 -> 409 us (micro/roll_ahead_b200.txt)
+#endif
 #ifndef PI2_ROLL1_UNROLL
 #define PI2_ROLL1_UNROLL 1  // t-loop unroll of rollout_kernel (2 / 4 within noise at C4: micro/roll_unroll_b200.txt)
 #endif
@@ -646,21 +650,45 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   // the analytic model's input row of step t + 1 is this step's post-step attitude row
   const bool hybrid = model == PI2_MODEL_HYBRID_LWPR;
   const bool with_std = hybrid && (a.spread || a.penalty);
+  // ap_row(t): the post-step attitude row of step t (xin row t + 1; the last step's from ang_last)
+  auto ap_row = [&](int t) { return (t + 1 < N) ? __ldcg(a.xin + (int64_t)(t + 1) * a.K + k) : __ldcg(a.ang_last + k); };
   float3 m4n = make_float3(0.f, 0.f, 0.f), s4n = m4n;
   if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, k);
   if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, k);
-  float4 apn = (1 < N) ? __ldcg(a.xin + a.K + k) : __ldcg(a.ang_last + k);
+  float4 apn = ap_row(0);
+#if PI2_ROLL1_AHEAD >= 2
+  // a second row set in flight: one step of this warp's work does not cover the DRAM latency
+  // (C4: 35 % of the stall samples sat on the first use of the one-ahead row)
+  float3 m4nn = m4n, s4nn = s4n;
+  float4 apnn = apn;
+  if (1 < N) {
+    if (hybrid) m4nn = ld_planes(a.lw_mean, a.lw_plane, a.K + k);
+    if (with_std) s4nn = ld_planes(a.lw_std, a.lw_plane, a.K + k);
+    apnn = ap_row(1);
+  }
+#endif
   float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldcg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll(kRoll1Unroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
     const float3 m4 = m4n, s4 = s4n;
     const float4 ap = apn;
+#if PI2_ROLL1_AHEAD >= 2
+    m4n = m4nn;
+    s4n = s4nn;
+    apn = apnn;
+    if (t + 2 < N) {
+      if (hybrid) m4nn = ld_planes(a.lw_mean, a.lw_plane, row + 2 * a.K);
+      if (with_std) s4nn = ld_planes(a.lw_std, a.lw_plane, row + 2 * a.K);
+      apnn = ap_row(t + 2);
+    }
+#else
     if (t + 1 < N) {
       if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
       if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
-      apn = (t + 2 < N) ? __ldcg(a.xin + row + 2 * a.K) : __ldcg(a.ang_last + k);
+      apn = ap_row(t + 1);
     }
+#endif
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};
     if (hybrid) {
       mn[0] = m4.x; mn[1] = m4.y; mn[2] = m4.z;
