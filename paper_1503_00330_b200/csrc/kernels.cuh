@@ -1378,11 +1378,9 @@ __global__ void apply_root_kernel(const double *__restrict__ root, int N, double
 // ---------------------------------------------------------------------------
 __device__ void smem_tree(double (*v)[PI2_PARTIAL_WIDTH], int n, double neg_inv) {
   for (int st = 1; st < n; st <<= 1) {
-    const int pairs = (n + 2 * st - 1) / (2 * st);
-    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
-      const int i = p * 2 * st;
-      if (i + st < n) partial_combine(v[i], v[i + st], neg_inv);
-    }
+    // pair p = (v[2 st p], v[2 st p + st]); thread p, p + blockDim, ... (no division)
+    for (int i = 2 * st * (int)threadIdx.x; i + st < n; i += 2 * st * (int)blockDim.x)
+      partial_combine(v[i], v[i + st], neg_inv);
     __syncthreads();
   }
 }
@@ -1399,9 +1397,14 @@ __global__ void __launch_bounds__(256)
   for (int64_t s = 0; s < nseg; ++s) {
     const int cnt = (int)(n - s * kSeg < kSeg ? n - s * kSeg : kSeg);
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const double *src = leaves + ((s * kSeg + i) * N + t) * PI2_PARTIAL_WIDTH;
+      // a leaf's 6 doubles are 48 contiguous, 16-byte aligned bytes: three 128-bit loads
+      const double2 *src = reinterpret_cast<const double2 *>(leaves + ((s * kSeg + i) * N + t) * PI2_PARTIAL_WIDTH);
 #pragma unroll
-      for (int c = 0; c < PI2_PARTIAL_WIDTH; ++c) seg[i][c] = __ldcg(src + c);  // coherent (see pdl_wait)
+      for (int c = 0; c < PI2_PARTIAL_WIDTH / 2; ++c) {
+        const double2 v = __ldcg(src + c);  // coherent (see pdl_wait)
+        seg[i][2 * c] = v.x;
+        seg[i][2 * c + 1] = v.y;
+      }
     }
     __syncthreads();
     smem_tree(seg, cnt, neg_inv);
