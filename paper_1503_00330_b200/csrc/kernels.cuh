@@ -1385,7 +1385,8 @@ __device__ void smem_tree(double (*v)[PI2_PARTIAL_WIDTH], int n, double neg_inv)
   }
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kCombineThreads = 256;
+__global__ void __launch_bounds__(kCombineThreads)
     combine_kernel(const double *__restrict__ leaves, int64_t n, int N, double neg_inv,
                    double *__restrict__ root_out, double *__restrict__ plan, DynParams dp, double *plan_host) {
   extern __shared__ double cmb[];
@@ -1394,19 +1395,37 @@ __global__ void __launch_bounds__(256)
   pdl_wait();
   const int t = blockIdx.x;
   const int64_t nseg = (n + kSeg - 1) / kSeg;
-  for (int64_t s = 0; s < nseg; ++s) {
+  // the next segment's leaves are loaded into registers while this one's tree runs
+  // (blockDim = kCombineThreads: kSeg / kCombineThreads leaves per thread); a leaf's 6
+  // doubles are 48 contiguous, 16-byte aligned bytes: three 128-bit loads
+  constexpr int LPT = kSeg / kCombineThreads;
+  double2 nx[LPT][PI2_PARTIAL_WIDTH / 2];
+  auto load_seg = [&](int64_t s) {
     const int cnt = (int)(n - s * kSeg < kSeg ? n - s * kSeg : kSeg);
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      // a leaf's 6 doubles are 48 contiguous, 16-byte aligned bytes: three 128-bit loads
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int i = (int)threadIdx.x + j * kCombineThreads;
+      if (i >= cnt) break;
       const double2 *src = reinterpret_cast<const double2 *>(leaves + ((s * kSeg + i) * N + t) * PI2_PARTIAL_WIDTH);
 #pragma unroll
+      for (int c = 0; c < PI2_PARTIAL_WIDTH / 2; ++c) nx[j][c] = __ldcg(src + c);  // coherent (see pdl_wait)
+    }
+  };
+  load_seg(0);
+  for (int64_t s = 0; s < nseg; ++s) {
+    const int cnt = (int)(n - s * kSeg < kSeg ? n - s * kSeg : kSeg);
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int i = (int)threadIdx.x + j * kCombineThreads;
+      if (i >= cnt) break;
+#pragma unroll
       for (int c = 0; c < PI2_PARTIAL_WIDTH / 2; ++c) {
-        const double2 v = __ldcg(src + c);  // coherent (see pdl_wait)
-        seg[i][2 * c] = v.x;
-        seg[i][2 * c + 1] = v.y;
+        seg[i][2 * c] = nx[j][c].x;
+        seg[i][2 * c + 1] = nx[j][c].y;
       }
     }
     __syncthreads();
+    if (s + 1 < nseg) load_seg(s + 1);
     smem_tree(seg, cnt, neg_inv);
     if (threadIdx.x == 0) {
 #pragma unroll

@@ -641,7 +641,7 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
   if ((n + kSeg - 1) / kSeg > kSeg) return fail(ctx, PI2_ERR_INVALID, "too many partials (%lld)", (long long)n);
   const int smem = 2 * kSeg * PI2_PARTIAL_WIDTH * (int)sizeof(double);
   TRY(set_smem(ctx, combine_kernel, smem));
-  TRY(launch_pdl_if(after_kernel, ctx, combine_kernel, dim3(N), dim3(256), smem, st, leaves, n, N, neg_inv, root, plan,
+  TRY(launch_pdl_if(after_kernel, ctx, combine_kernel, dim3(N), dim3(kCombineThreads), smem, st, leaves, n, N, neg_inv, root, plan,
                     ctx->dp, plan_host));
   CU(cudaGetLastError());
   return PI2_OK;
