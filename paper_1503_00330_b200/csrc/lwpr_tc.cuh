@@ -64,6 +64,7 @@ struct LwprTcArgs {
   float *mean_out, *sd_out;  // planes: axis c of row r at [c * plane + r]
   int64_t plane;
   int sqrt_out;
+  int sms;  // SM count: the MMA-issuing warp rotates over the co-resident CTAs (PI2_TC_ROTATE)
 };
 
 // byte offset of element (row, k) in a K-major no-swizzle operand, K = 8 (fp32/tf32)
@@ -235,6 +236,10 @@ __device__ __forceinline__ void tc_trace(int slot, int &n, int i) {
 // 3xTF32 as TWO MMAs per chunk instead of three: the same product terms hi.hi + hi.lo +
 // lo.hi rearranged along K (A1 = [x~hi, 1, 1, q~hi, q~lo] . B1 = [Whi, A0hi, A0lo, 1, 1] and
 // A2 = [x~hi, x~lo] . B2 = [Wlo, Whi]); operands keep their sizes
+#ifndef PI2_TC_ROTATE  // 1: CTA b issues its MMAs from warp (b / SMs) % 4, so the co-resident CTAs'
+#define PI2_TC_ROTATE 0  // issuers sit on different SM sub-partitions (else all on warp 0's); no change:
+                         // C2 LWPR 393 vs 393 us, C4 step 6.06 vs 6.08 ms (micro/tc_rotate_b200.txt)
+#endif
 #ifndef PI2_TC_ELECT  // chunk MMAs issued by converged warp 0 with elect.sync (else thread 0)
 #define PI2_TC_ELECT 0  // 1 measured slower in situ: L=100 385 -> 400 us, L=200 677 -> 698 (micro/tc_elect_b200.txt)
 #endif
@@ -481,6 +486,8 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
   float *slv_base = sw + wfl;
   uint8_t *sa = tsm + (((wfl + nlv) * 4 + 127) / 128) * 128;  // two A operands
   const int tid = threadIdx.x, warp = tid >> 5;
+  // the thread that issues the chunk MMAs (and the TMA weight loads)
+  const int issuer = PI2_TC_ROTATE && a.sms > 0 ? 32 * (int)((blockIdx.x / (unsigned)a.sms) & 3u) : 0;
 
   if (!STREAM && !WBULK)
     for (int64_t i = tid; i < (wend - wbeg) / 4; i += blockDim.x)
@@ -506,7 +513,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   const uint32_t mbar_addr = (uint32_t)__cvta_generic_to_shared(&mbar);
-  if (tid == 0) {
+  if (tid == issuer) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_addr));
     if (STREAM || WBULK) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar_addr));
@@ -556,7 +563,7 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
   PI2_TC_TDECL
 
   // WBULK: the resident W landed (thread 0 issues every MMA)
-  if (WBULK && tid == 0 && tile < ntiles) mbar_wait(wbar_addr, 0);
+  if (WBULK && tid == issuer && tile < ntiles) mbar_wait(wbar_addr, 0);
   for (; tile < ntiles; tile += tstride, buf ^= 1) {
     const uint32_t sa_addr = (uint32_t)__cvta_generic_to_shared(sa + buf * kTcABytes);
     float2 den = make_float2(0.f, 0.f), num = den, m2 = den, lv = den;
@@ -587,10 +594,10 @@ __device__ __forceinline__ void lwpr_tc_body(const LwprTcArgs &a, uint8_t *tsm, 
 #endif
         mma_commit_elect(mbar_addr);
         // the other slot held chunk nw - 1, whose MMA completed before this chunk's barrier
-        if (STREAM && tid == 0 && (c + 1 < nch || tile + tstride < ntiles)) load_w(c + 1 < nch ? c + 1 : 0, (nw + 1) & 1);
+        if (STREAM && tid == issuer && (c + 1 < nch || tile + tstride < ntiles)) load_w(c + 1 < nch ? c + 1 : 0, (nw + 1) & 1);
       }
 #else
-      if (tid == 0) {
+      if (tid == issuer) {
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t idesc = umma_idesc_tf32(128, 2 * lc);
         const uint64_t a_hi = umma_smem_desc(sa_addr), a_lo = umma_smem_desc(sa_addr + 4096);

@@ -266,6 +266,7 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
   a.sqrt_out = 1;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  a.sms = sms;
   const int64_t tiles = (rows + 127) / 128;
   const int64_t per_axis = std::min<int64_t>((int64_t)kTcCtasPerSm * sms / 3, tiles);
   const int64_t grid = per_axis * 3;  // CTA i -> axis i % 3
