@@ -140,7 +140,8 @@ int pi2_set_cost(pi2_ctx *ctx, const pi2_cost *cost);
 /* The navigation cost's full obstacle list, any length (RolloutCost.obstacles,
  * simworld.py:141-146, has no limit; pi2_cost holds PI2_MAX_OBSTACLES): (n, 2)
  * float32 (x, y), summed in list order like simworld.py:188-190.  Call after
- * pi2_set_cost (which resets the list to the struct's). */
+ * pi2_set_cost (which resets the list to the struct's).  When the part past
+ * the struct changes, the call synchronises the device before restaging it. */
 int pi2_set_cost_obstacles(pi2_ctx *ctx, int32_t n, const float *obstacles_xy);
 
 /* ---- hot path ----------------------------------------------------------- */
