@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) fused_step_kernel(co
     };
     // sub-rollouts of step t (rollout_kernel<MM, FAST>'s arithmetic); pad: the next input
     // row's thrust (0 after the last step), consumed as the unfused kernels do
+    DynDraws draws[MM];  // dynamics draws carried between steps (kernels.cuh DynDraws)
     auto rollout_step = [&](int t, float pad) {
       float mn[3], sd[3];
 #pragma unroll
@@ -201,10 +202,11 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm) fused_step_kernel(co
         if (m >= S) break;
         float acc[3];
         if (f.spread) {
-          const float4 z = normals4((kg * (uint64_t)f.M + (uint64_t)m) * (uint64_t)N + (uint64_t)t, dkey.k0, dkey.k1);
-          acc[0] = __fadd_rn(__fmul_rn(sd[0], z.x), mn[0]);
-          acc[1] = __fadd_rn(__fmul_rn(sd[1], z.y), mn[1]);
-          acc[2] = __fadd_rn(__fmul_rn(sd[2], z.z), mn[2]);
+          float z[3];
+          draws[m].next((kg * (uint64_t)f.M + (uint64_t)m) * (uint64_t)dyn_blocks(N), t, dkey.k0, dkey.k1, z);
+          acc[0] = __fadd_rn(__fmul_rn(sd[0], z[0]), mn[0]);
+          acc[1] = __fadd_rn(__fmul_rn(sd[1], z[1]), mn[1]);
+          acc[2] = __fadd_rn(__fmul_rn(sd[2], z[2]), mn[2]);
         } else {
           acc[0] = mn[0]; acc[1] = mn[1]; acc[2] = mn[2];
         }

@@ -84,6 +84,55 @@ __device__ __forceinline__ void device_eps(const StepArgs *sa, Key128 key, uint6
   eps_from_z(sa, device_z(key, kg, N, t), e);
 }
 
+// Dynamics draws of the device stream: sub-rollout (k, m) consumes the normals of its
+// Philox blocks in order, all four of each, 3 per step — step t takes normals 3t .. 3t+2
+// of the sequence normals4(base + 0), normals4(base + 1), ... with base = (k M + m) * NB
+// and NB = dyn_blocks(N) blocks per sub-rollout (4 steps per 3 blocks; tests/devnoise.py
+// replicates it).
+__host__ __device__ __forceinline__ int64_t dyn_blocks(int N) { return (3 * (int64_t)N + 3) / 4; }
+
+// step t's three draws without state (two blocks when they straddle a block boundary)
+__device__ __forceinline__ void dyn3(uint64_t base, int t, uint64_t k0, uint64_t k1, float d[3]) {
+  const int64_t q = 3 * (int64_t)t;
+  const int r = (int)(q & 3);
+  const float4 z = normals4(base + (uint64_t)(q >> 2), k0, k1);
+  const float v0[4] = {z.x, z.y, z.z, z.w};
+  if (r <= 1) {
+    d[0] = v0[r]; d[1] = v0[r + 1]; d[2] = v0[r + 2];
+    return;
+  }
+  const float4 y = normals4(base + (uint64_t)(q >> 2) + 1, k0, k1);
+  if (r == 2) {
+    d[0] = z.z; d[1] = z.w; d[2] = y.x;
+  } else {
+    d[0] = z.w; d[1] = y.x; d[2] = y.y;
+  }
+}
+
+// the same draws for t = 0, 1, 2, ... in order: one Philox block per step for three steps
+// of four, the leftover normals carried (the round-1 stream used 3 of 4 normals per block)
+struct DynDraws {
+  float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+  __device__ __forceinline__ void next(uint64_t base, int t, uint64_t k0, uint64_t k1, float d[3]) {
+    const int ph = t & 3;
+    if (ph == 3) {
+      d[0] = c0; d[1] = c1; d[2] = c2;
+      return;
+    }
+    const float4 z = normals4(base + (uint64_t)(3 * (t >> 2) + ph), k0, k1);
+    if (ph == 0) {
+      d[0] = z.x; d[1] = z.y; d[2] = z.z;
+      c0 = z.w;
+    } else if (ph == 1) {
+      d[0] = c0; d[1] = z.x; d[2] = z.y;
+      c0 = z.z; c1 = z.w;
+    } else {
+      d[0] = c0; d[1] = c1; d[2] = z.x;
+      c0 = z.y; c1 = z.z; c2 = z.w;
+    }
+  }
+};
+
 // np.clip(v, lo, hi, out=...) with array bounds (controller.py:259, :371): numpy's
 // _NPY_MAX/_NPY_MIN, i.e. NaN propagates and max(-0, +0) = +0 ((a > b) ? a : b).
 // Two compare-selects, against ~18 SASS instructions for the fmin/fmax pair.
@@ -725,8 +774,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
       if (a.spread) {
         float d[3];
         if (a.device_dyn) {
-          const float4 z = normals4((kg * (uint64_t)M + (uint64_t)m) * (uint64_t)N + (uint64_t)t, dk0, dk1);
-          d[0] = z.x; d[1] = z.y; d[2] = z.z;
+          dyn3((kg * (uint64_t)M + (uint64_t)m) * (uint64_t)dyn_blocks(N), t, dk0, dk1, d);
         } else {
           const float *dp = a.dyn + ((k * M + m) * (int64_t)N + t) * 3;
           d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
@@ -848,8 +896,10 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   const int64_t kk = live ? k : 0;
   const bool device_dyn = FAST || a.device_dyn;
   const bool two_point = !FAST && a.model == PI2_MODEL_TWO_POINT;
-  // counter of (k, m, t=0) of each slot's sub-rollout m = lane_g + j * GL
-  const uint64_t dyn_base = (kg * (uint64_t)S + (uint64_t)lane_g) * (uint64_t)N;
+  // first Philox block of each slot's sub-rollout m = lane_g + j * GL (DynDraws)
+  const uint64_t nb = (uint64_t)dyn_blocks(N);
+  const uint64_t dyn_base = (kg * (uint64_t)S + (uint64_t)lane_g) * nb;
+  DynDraws draws[SPL];
 
   float cs[SPL][3], ccs[SPL][3];
   bool crashed[SPL];
@@ -908,8 +958,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
         const int m = lane_g + j * GL;
         float d[3];
         if (device_dyn) {
-          const float4 z = normals4(dyn_base + (uint64_t)(j * GL) * (uint64_t)N + (uint64_t)t, dk0, dk1);
-          d[0] = z.x; d[1] = z.y; d[2] = z.z;
+          draws[j].next(dyn_base + (uint64_t)(j * GL) * nb, t, dk0, dk1, d);
         } else {
           const float *dp = a.dyn + ((kk * S + m) * (int64_t)N + t) * 3;
           d[0] = __ldg(dp); d[1] = __ldg(dp + 1); d[2] = __ldg(dp + 2);
@@ -1473,12 +1522,14 @@ __global__ void noise_kernel(const StepArgs *__restrict__ sa, int which, uint64_
     for (int c = 0; c < 4; ++c) eps_out[i * 4 + c] = e[c];
   } else {
     if (i >= K * M * N) return;  // i = (k * M + m) * N + t
-    const uint64_t kg_idx = (uint64_t)(k_off * M * N + i);
+    const int t = (int)(i % N);
+    const uint64_t km = (uint64_t)(k_off * M + i / N);  // global (k, m)
     const Key128 dk = iter_key(sa->key_prefix[1], iteration);
-    const float4 z = normals4(kg_idx, dk.k0, dk.k1);
-    dyn_out[i * 3 + 0] = z.x;
-    dyn_out[i * 3 + 1] = z.y;
-    dyn_out[i * 3 + 2] = z.z;
+    float d[3];
+    dyn3(km * (uint64_t)dyn_blocks(N), t, dk.k0, dk.k1, d);
+    dyn_out[i * 3 + 0] = d[0];
+    dyn_out[i * 3 + 1] = d[1];
+    dyn_out[i * 3 + 2] = d[2];
   }
 }
 

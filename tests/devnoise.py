@@ -71,7 +71,13 @@ def control_noise(seed, cycle, iteration, K, N, std, k_off=0):
 
 
 def dynamics_noise(seed, cycle, iteration, K, M, N, k_off=0):
-    """z (K, M, N, 3) of the dynamics stream (rollout kernels / noise_kernel)."""
+    """z (K, M, N, 3) of the dynamics stream (rollout kernels / noise_kernel): sub-rollout
+    (k, m) reads its Philox blocks (k M + m) * NB + j, j < NB = ceil(3N / 4), as one
+    sequence of normals, all four of each block, and step t takes normals 3t .. 3t + 2
+    (csrc/kernels.cuh DynDraws / dyn3)."""
     key = rng.derive_key(seed, rng.STREAM_DYNAMICS, cycle, iteration)
-    idx = np.arange(k_off * M * N, (k_off + K) * M * N, dtype=np.uint64)
-    return normals4(idx, key)[:, :3].reshape(K, M, N, 3)
+    nb = (3 * N + 3) // 4
+    km = np.arange(k_off * M, (k_off + K) * M, dtype=np.uint64)
+    idx = (km[:, None] * np.uint64(nb) + np.arange(nb, dtype=np.uint64)[None, :]).reshape(-1)
+    seq = normals4(idx, key).reshape(K * M, 4 * nb)[:, :3 * N]
+    return seq.reshape(K, M, N, 3)

@@ -29,3 +29,26 @@ def test_replica_streams_are_standard_normal_and_addressed():
     np.testing.assert_array_equal(devnoise.control_noise(7, 3, 1, 500, 50, std, k_off=1500), e[1500:])
     z = devnoise.dynamics_noise(7, 3, 1, 300, 4, 50)
     np.testing.assert_allclose(z.std(), 1.0, atol=0.02)
+
+
+def test_dynamics_stream_uses_all_four_normals_of_each_block():
+    """Dynamics draws: sub-rollout (k, m) reads its Philox blocks as one sequence, all
+    four normals of each (csrc/kernels.cuh DynDraws), 3 per step; shards read the same
+    numbers as the whole population."""
+    from paper_1503_00330_b200 import rng
+
+    K, M, N = 3, 2, 8  # N = 8: 6 blocks of 4 = 24 normals, all of them used
+    z = devnoise.dynamics_noise(5, 2, 0, K, M, N)
+    key = rng.derive_key(5, rng.STREAM_DYNAMICS, 2, 0)
+    nb = (3 * N + 3) // 4
+    assert nb * 4 == 3 * N
+    for k in range(K):
+        for m in range(M):
+            base = (k * M + m) * nb
+            seq = devnoise.normals4(np.arange(base, base + nb, dtype=np.uint64), key).reshape(-1)
+            np.testing.assert_array_equal(z[k, m].reshape(-1), seq)
+    np.testing.assert_array_equal(devnoise.dynamics_noise(5, 2, 0, 1, M, N, k_off=2), z[2:])
+    # an odd horizon: the last block's trailing normals are the only ones left unused
+    z5 = devnoise.dynamics_noise(5, 2, 0, 1, 1, 5)
+    seq = devnoise.normals4(np.arange(0, 4, dtype=np.uint64), key).reshape(-1)
+    np.testing.assert_array_equal(z5[0, 0].reshape(-1), seq[:15])
