@@ -1235,10 +1235,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 #ifndef PI2_PARTIALS_ZAHEAD
-#define PI2_PARTIALS_ZAHEAD 2  // stored-normal loads issued this many elements ahead (0: in the loop);
-                               // C2 partials 32 -> 26 us, C4 379 -> 285 us; 4 (70 regs) 28 / 330 us (micro/partials_zahead_b200.txt)
+#define PI2_PARTIALS_ZAHEAD 3  // stored-normal loads issued this many elements ahead (0: in the loop);
+                               // C4 partials 379 (0) / 285 (2) / 252 (3, 64 regs) us; 4 needs > 64 regs
+                               // (3 blocks/SM): 330 us (micro/partials_zahead_b200.txt)
 #endif
+#ifndef PI2_PARTIALS_MINB
+#define PI2_PARTIALS_MINB 0  // > 0: __launch_bounds__ minimum blocks per SM (register cap)
+#endif
+#if PI2_PARTIALS_MINB > 0
+__global__ void __launch_bounds__(32 * kChunkWarps, PI2_PARTIALS_MINB)
+#else
 __global__ void __launch_bounds__(32 * kChunkWarps)
+#endif
     partials_kernel(const double *__restrict__ costs, int64_t cs_k, int64_t cs_t,
                     const double *__restrict__ eps, const float4 *zin, const StepArgs *__restrict__ sa, int iteration,
                     int64_t K, int64_t k_off, int N, double neg_inv, double *__restrict__ out) {
