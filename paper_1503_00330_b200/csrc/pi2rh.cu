@@ -76,6 +76,7 @@ struct pi2_ctx {
   uint8_t *d_crash = nullptr;
   double *d_partials = nullptr, *d_root = nullptr;
   float4 *d_z = nullptr;  // device-noise exploration normals z(k, t) at [t * K + k] (attitude -> partials)
+  bool store_z = true;    // PI2_STORE_Z=0: the partials kernel regenerates z instead (experiments)
   int64_t n_chunks = 0;
   // lazily grown scratch
   double *d_noise = nullptr;
@@ -561,7 +562,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
       TRY(set_smem(ctx, attitude_wide_kernel<true>, wsmem));
       TRY(launch_pdl_if(att_pdl, ctx, attitude_wide_kernel<true>, dim3(wgrid), dim3(32 * kWideWarps), wsmem, st, ctx->d_args,
                      ctx->d_plan, nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin,
-                     ctx->d_ang_last, ctx->d_z));
+                     ctx->d_ang_last, ctx->store_z ? ctx->d_z : nullptr));
     }
   } else if (noise_dev) {
     TRY(set_smem(ctx, attitude_kernel<false>, psmem));
@@ -571,7 +572,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
   } else {
     TRY(set_smem(ctx, attitude_kernel<true>, psmem));
     TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
-                   nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, ctx->d_z));
+                   nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, ctx->store_z ? ctx->d_z : nullptr));
   }
   CU(cudaGetLastError());
   if (ev) CU(cudaEventRecord(ev[1], st));
@@ -652,7 +653,7 @@ int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double 
 int launch_iteration(pi2_ctx *ctx, int it, double neg_inv, double *root, bool update_plan,
                      cudaStream_t st, double *plan_host = nullptr, bool att_pdl = false) {
   TRY(launch_rollouts(ctx, it, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, nullptr, att_pdl));
-  TRY(launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->d_z, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+  TRY(launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->store_z ? ctx->d_z : nullptr, it, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
                       ctx->d_partials, st, true));
   return launch_combine(ctx, ctx->d_partials, ctx->n_chunks, ctx->N, neg_inv, root,
                         update_plan ? ctx->d_plan : nullptr, st, true, plan_host);
@@ -743,6 +744,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
   if (const char *e = getenv("PI2_WIDE_MAX_K")) ctx->wide_max_k = std::atoll(e);
   if (const char *e = getenv("PI2_TC_BULK_MAX_TILES")) ctx->tc_bulk_max_tiles = std::atoll(e);
   if (const char *e = getenv("PI2_FUSED")) ctx->fused = std::atoi(e);
+  if (const char *e = getenv("PI2_STORE_Z")) ctx->store_z = std::atoi(e) != 0;
   if (const char *e = getenv("PI2_SMEM_HORIZON")) ctx->smem_horizon = std::min(std::atoi(e), kSmemHorizon);
   {
     int uva = 0;
@@ -1251,7 +1253,7 @@ int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t r
     rc = launch_rollouts(ctx, 0, nullptr, nullptr, ctx->d_costs, ctx->d_crash, st, ev);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[3], st);
-    rc = launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->d_z, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
+    rc = launch_partials(ctx, ctx->d_costs, 1, ctx->K, nullptr, ctx->store_z ? ctx->d_z : nullptr, 0, ctx->K, ctx->dims.rollout_offset, ctx->N, neg_inv,
                          ctx->d_partials, st, false);
     if (rc != PI2_OK) break;
     cudaEventRecord(ev[4], st);
