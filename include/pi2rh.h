@@ -33,7 +33,7 @@ extern "C" {
 
 #define PI2_ABI_VERSION 1
 #define PI2_MAX_OBSTACLES 16
-#define PI2_MAX_SUB_ROLLOUTS 64
+#define PI2_MAX_SUB_ROLLOUTS 256
 #define PI2_PARTIAL_WIDTH 6 /* (min S, Z, V[4]) per timestep, float64 */
 
 /* status codes */

@@ -20,7 +20,7 @@ MODEL_HYBRID_LWPR, MODEL_ANALYTIC, MODEL_TWO_POINT = 1, 2, 3
 COST_NAVIGATION, COST_THRESHOLD = 0, 1
 STREAM_CONTROL, STREAM_DYNAMICS = 1, 2
 MAX_OBSTACLES = 16
-MAX_SUB_ROLLOUTS = 64
+MAX_SUB_ROLLOUTS = 256
 PARTIAL_WIDTH = 6
 
 

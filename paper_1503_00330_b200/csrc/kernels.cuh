@@ -659,7 +659,7 @@ constexpr int kRoll1Unroll = PI2_ROLL1_UNROLL;
 // FAST: hybrid LWPR model + navigation cost, branches folded at compile time.
 template <int MM, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
-  constexpr int MCAP = MM > 0 ? MM : PI2_MAX_SUB_ROLLOUTS;
+  constexpr int MCAP = MM > 0 ? MM : 64;  // MM = 0 (runtime M) is not instantiated: S > 1 runs the group kernel
   extern __shared__ float sq[];  // (N, blockDim): this thread's stage costs, column tid
   __shared__ pi2_cost cost;
   if (threadIdx.x == 0) cost = a.sa->cost;
@@ -852,8 +852,8 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
 constexpr int kRollUnroll = PI2_ROLL_UNROLL;
 
 // Sub-rollouts on lanes: a group of G lanes (G = S rounded up to a power of
-// two, <= 32) per rollout, lane m integrating sub-rollout m; G = 64 (33 <= S
-// <= 64) runs 32 lanes holding sub-rollouts m and m + 32 each.  The M-mean is
+// two, <= 32) per rollout, lane m integrating sub-rollout m; G = 64 .. 256
+// (33 <= S <= 256) runs 32 lanes holding sub-rollouts m, m + 32, ... each.  The M-mean is
 // the reference's pairwise tree (controller.py:314-319): for S == G an xor
 // butterfly reproduces it exactly (adjacent pairs at every level, IEEE add
 // is commutative; with two slots per lane the butterfly leaves the means of
@@ -864,7 +864,7 @@ constexpr int kRollUnroll = PI2_ROLL_UNROLL;
 // real-time configuration) with every branch folded at compile time.
 template <int G, bool FAST>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a) {
-  constexpr int SPL = G > 32 ? 2 : 1;     // sub-rollouts per lane
+  constexpr int SPL = G > 32 ? G / 32 : 1;  // sub-rollouts per lane (G = 64 .. 256: 32 lanes)
   constexpr int GL = G / SPL;             // lanes per rollout
   constexpr int RPB = kRolloutBlock / GL;  // rollouts per block
   extern __shared__ float sq[];           // (N, RPB) stage costs
@@ -992,7 +992,35 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
 #pragma unroll
         for (int off = 1; off < GL; off <<= 1)
           q[j] = __fmul_rn(0.5f, __fadd_rn(q[j], __shfl_xor_sync(0xffffffffu, q[j], off)));
-      qm = SPL == 1 ? q[0] : __fmul_rn(0.5f, __fadd_rn(q[0], q[SPL - 1]));
+      // the tree's upper levels pair adjacent 32-blocks: slots (j, j + w)
+#pragma unroll
+      for (int w = 1; w < SPL; w <<= 1)
+#pragma unroll
+        for (int j = 0; j + w < SPL; j += 2 * w) q[j] = __fmul_rn(0.5f, __fadd_rn(q[j], q[j + w]));
+      qm = q[0];
+    } else if (G > 64) {  // replay the reference loop in place in shared memory (one lane)
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) qbuf[j * kRolloutBlock + threadIdx.x] = q[j];
+      __syncwarp();
+      qm = 0.0f;
+      if (lane_g == 0) {
+        // element i of this rollout's sub-rollout costs: slot i / 32, lane i % 32
+        auto at = [&](int i) -> float & { return qbuf[(i / GL) * kRolloutBlock + threadIdx.x + i % GL]; };
+        int n = S;
+        while (n > 1) {
+          if ((n & 1) == 0) {
+            for (int i = 0; i < n / 2; ++i) at(i) = __fmul_rn(0.5f, __fadd_rn(at(2 * i), at(2 * i + 1)));
+            n >>= 1;
+          } else {
+            float sum = at(0);
+            for (int i = 1; i < n; ++i) sum = __fadd_rn(sum, at(i));
+            at(0) = __fdiv_rn(sum, (float)n);
+            n = 1;
+          }
+        }
+        qm = at(0);
+      }
+      __syncwarp();
     } else {
 #pragma unroll
       for (int j = 0; j < SPL; ++j) qbuf[j * kRolloutBlock + threadIdx.x] = q[j];

@@ -392,7 +392,7 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
   const bool nav = ctx->cost.kind == PI2_COST_NAVIGATION && struct_obstacles(ctx);  // FAST-eligible
   const bool hybrid = a.model == PI2_MODEL_HYBRID_LWPR;
   // sub-rollouts on lanes (any model but the analytic one, which is never spread);
-  // 33..64 on 32 lanes with two each (S <= PI2_MAX_SUB_ROLLOUTS = 64)
+  // 33..256 on 32 lanes with S / 32 rounded up to a power of two each (S <= PI2_MAX_SUB_ROLLOUTS)
   if (S > 1) {
     const bool fast = hybrid && nav && a.device_dyn;
     if (S <= 2) return launch_group_g<2>(ctx, a, fast, st);
@@ -400,7 +400,9 @@ int launch_rollout(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
     if (S <= 8) return launch_group_g<8>(ctx, a, fast, st);
     if (S <= 16) return launch_group_g<16>(ctx, a, fast, st);
     if (S <= 32) return launch_group_g<32>(ctx, a, fast, st);
-    return launch_group_g<64>(ctx, a, fast, st);
+    if (S <= 64) return launch_group_g<64>(ctx, a, fast, st);
+    if (S <= 128) return launch_group_g<128>(ctx, a, fast, st);
+    return launch_group_g<256>(ctx, a, fast, st);
   }
   if (S == 1 && a.K <= ctx->wide_max_k && a.N <= ctx->smem_horizon) {  // latency regime: a warp per rollout
     const unsigned grid = (unsigned)((a.K + kWideWarps - 1) / kWideWarps);

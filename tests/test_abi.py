@@ -50,7 +50,7 @@ def test_invalid_dims_rejected_before_device_lookup():
     with pytest.raises(ValueError, match=">= 1"):
         _abi.Context(0, 0, 4, 1)
     with pytest.raises(ValueError, match="sub_rollouts"):
-        _abi.Context(0, 8, 4, 65)
+        _abi.Context(0, 8, 4, 257)
 
 
 def test_host_partials_reproduce_update():

@@ -146,3 +146,26 @@ def test_c5_largest_k_sampled():
     """C5 at its largest K (2^22, L=200): 65,536 rollouts in 8 blocks spread over the
     batch, including the last ones (float4 row indices beyond 2^31 / 16 bytes)."""
     sampled_check(1 << 22, 50, 200, 1, 65536, blocks=8)
+
+
+@pytest.mark.parametrize("M", [100, 128, 200, 256])
+def test_many_sub_rollouts_match_oracle(M):
+    """M up to PI2_MAX_SUB_ROLLOUTS = 256 (32 lanes x up to 8 sub-rollouts per rollout; the
+    reference has no limit): the device-noise iteration's costs and crash flags against
+    the oracle on the same (materialised) noise, power-of-two M (butterfly + slot tree)
+    and not (the reference loop replayed in shared memory); ragged K."""
+    K, N, L = 700, 16, 24
+    stacks, model, cfg, state, plan, cost = setup(K, N, L, M)
+    eng = P.RolloutEngine(model, cfg, device=0, noise="device")
+    eng.optimize_device(state, plan, cost, cycle_index=CYCLE)  # binds and stages the context
+    ctx = eng.context(K, N)
+    costs_d, crash_d = device_costs(ctx, cfg, state, plan, K, N)
+    eps, dyn = device_noise(ctx, cfg, K, N, M)
+    rc, rf, _, _ = oracle_eval(stacks, state, plan, eps, dyn, M, chunk=128)
+    check_costs(costs_d.cpu().numpy(), crash_d.cpu().numpy().astype(bool), rc, rf)
+    # host-noise evaluate through the engine API (the reference's own sampled streams)
+    hb = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, P.sample_noise(cfg, 1, 0), cost,
+                                                       P.sample_dynamics_noise(cfg, 1, 0))
+    rc2, rf2, _, _ = oracle_eval(stacks, state, plan, P.sample_noise(cfg, 1, 0), P.sample_dynamics_noise(cfg, 1, 0), M,
+                                 chunk=128)
+    check_costs(hb.costs_to_go, hb.crash_flags, rc2, rf2)

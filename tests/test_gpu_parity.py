@@ -289,10 +289,10 @@ def test_two_point_model_matches_enumeration():
 
 
 def test_subrollout_cost_variance_scales_inverse_m():
-    """Reference test_controller.py:308-327 on the GPU engine (M=64 uses the generic kernel)."""
+    """Reference test_controller.py:308-327 on the GPU engine (M=64 and 256: several sub-rollouts per lane)."""
     p = P.QuadParams()
     stds = {}
-    for m_sub in (4, 16, 64):
+    for m_sub in (4, 16, 64, 256):
         cfg = P.PiConfig(num_rollouts=1500, horizon_steps=10, sub_rollouts=m_sub, rng_seed=3)
         dyn = P.sample_dynamics_noise(cfg, 0, 0)
         b = P.evaluate_rollouts(P.QuadState.hover((0, 0, 0)), P.ControlPlan.hover(p, 10), np.zeros((1500, 10, 4)),
@@ -300,6 +300,7 @@ def test_subrollout_cost_variance_scales_inverse_m():
         stds[m_sub] = b.costs_to_go[:, 0].std()
     assert stds[16] == pytest.approx(stds[4] / 2.0, rel=0.25)
     assert stds[64] == pytest.approx(stds[16] / 2.0, rel=0.25)
+    assert stds[256] == pytest.approx(stds[64] / 2.0, rel=0.25)
 
 
 def test_engine_errors_match_reference():
