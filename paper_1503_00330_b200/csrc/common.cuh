@@ -24,7 +24,7 @@ constexpr int kSeg = 1024;          // leaves per combine segment
 constexpr int kMaxSmallM = 8;       // sub-rollouts held in registers
 constexpr int kSmemHorizon = 400;     // up to this many steps the rollout kernels keep stage costs in shared
                                       // memory and the warp-per-rollout kernels are eligible
-constexpr int kMaxHorizon = 4096;     // pi2_create limit: the attitude kernel stages the plan in shared memory
+constexpr int kMaxHorizon = 4096;     // the attitude kernel stages the plan in shared memory up to this horizon
 constexpr int64_t kWideMaxK = 8192;  // up to this K, attitude/rollout use a warp per rollout (latency);
                                      // measured crossover ~8192 (profiles/micro/wide_threshold_b200.txt)
 constexpr double kPi = 3.141592653589793;        // np.pi

@@ -164,11 +164,15 @@ __global__ void __launch_bounds__(kRolloutBlock)
                     float4 *__restrict__ zout) {
   // zout (device noise): the exploration normals z(k, t) at zout[t * K + k] for the
   // partials kernel, which would otherwise regenerate them (e = z * std either way)
-  extern __shared__ double splan[];  // (N, 4)
+  extern __shared__ double smem_plan[];  // (N, 4) when N <= kMaxHorizon
   pdl_wait();     // the plan is the previous iteration's update
   pdl_trigger();  // one wave: the LWPR kernel's prologue may start on free SM resources
-  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) splan[i] = plan[i];
+  // longer horizons read the plan rows from global memory (one broadcast load per row)
+  const bool staged = N <= kMaxHorizon;
+  if (staged)
+    for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) smem_plan[i] = plan[i];
   __syncthreads();
+  const double *splan = staged ? smem_plan : plan;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   double ang[3] = {sa->state[6], sa->state[7], sa->state[8]};

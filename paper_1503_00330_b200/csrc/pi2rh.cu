@@ -551,7 +551,7 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
     }
   }
   const unsigned grid = (unsigned)((K + kRolloutBlock - 1) / kRolloutBlock);
-  const int psmem = 4 * N * (int)sizeof(double);
+  const int psmem = N <= kMaxHorizon ? 4 * N * (int)sizeof(double) : 0;  // plan rows staged up to kMaxHorizon
   if (K <= ctx->wide_max_k && N <= ctx->smem_horizon) {  // latency regime: a warp per rollout
     const unsigned wgrid = (unsigned)((K + kWideWarps - 1) / kWideWarps);
     const int wsmem = psmem + kWideWarps * 4 * N * (int)sizeof(double) + kWideWarps * (N + 1) * (int)sizeof(float4);
@@ -718,7 +718,7 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
     return fail(nullptr, PI2_ERR_INVALID, "num_rollouts, sub_rollouts, horizon_steps must be >= 1");
   if (dims->sub_rollouts > PI2_MAX_SUB_ROLLOUTS)
     return fail(nullptr, PI2_ERR_INVALID, "sub_rollouts must be <= %d", PI2_MAX_SUB_ROLLOUTS);
-  if (dims->horizon_steps > kMaxHorizon) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= %d", kMaxHorizon);
+  if (dims->horizon_steps > (1 << 24)) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= %d", 1 << 24);
   if (dims->rollout_offset < 0) return fail(nullptr, PI2_ERR_INVALID, "rollout_offset must be >= 0");
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
