@@ -7,6 +7,7 @@
 // constructor, lwpr.py:339-358) and stream-key hashing (rng.py:33-44).
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -21,6 +22,18 @@
 #include "kernels.cuh"
 #include "lwpr_tc.cuh"
 #include "fused.cuh"
+
+namespace {
+// NVTX range (header-only NVTX3: a no-op unless a tool such as ncu --nvtx or nsys is
+// attached): every C-ABI entry point and every stage launch is a named range, so a
+// profiler can filter by them (ncu --nvtx --nvtx-include "lwpr/").
+struct Range {
+  explicit Range(const char *name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range &) = delete;
+  Range &operator=(const Range &) = delete;
+};
+}  // namespace
 
 using namespace pi2;
 
@@ -291,6 +304,7 @@ int launch_lwpr_tc(pi2_ctx *ctx, int64_t rows, const float4 *x, float *mean_out,
 // pdl: the stream predecessor is the attitude kernel (rollout chain)
 int launch_lwpr(pi2_ctx *ctx, int a_begin, int a_end, int64_t rows, const float4 *x, float *mean_out,
                 float *sd_out, int row_stride, int64_t axis_stride, int sqrt_out, cudaStream_t st, bool pdl = false) {
+  Range range_("lwpr");
   TRY(ensure_params(ctx));
   // all three axes into planes (the rollout path): tensor cores when eligible
   // (shared metric, each axis' weights fit at full residency; PI2_LWPR_TC=0 disables)
@@ -538,6 +552,7 @@ int launch_fused(pi2_ctx *ctx, int mm, int iteration, double *costs, uint8_t *cr
 int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const float *dyn_dev,
                     double *costs, uint8_t *crash, cudaStream_t st, cudaEvent_t *ev = nullptr,
                     bool att_pdl = false) {
+  Range range_("rollouts");
   const int64_t K = ctx->K;
   const int N = ctx->N;
   if (!noise_dev && !dyn_dev) {  // device noise: the fused kernel when eligible
@@ -620,6 +635,7 @@ dim3 partials_grid(int64_t chunks, int N) {
 int launch_partials(pi2_ctx *ctx, const double *costs, int64_t cs_k, int64_t cs_t, const double *eps,
                     const float4 *zin, int it, int64_t K, int64_t k_off, int N, double neg_inv, double *out,
                     cudaStream_t st, bool pdl) {
+  Range range_("partials");
   const int64_t chunks = (K + kChunk - 1) / kChunk;
   const dim3 g = partials_grid(chunks, N);
   const bool split = ctx->partials_split == 2 || (ctx->partials_split == 1 && (int64_t)g.x * g.y < kPartialsSplitBlocks);
@@ -637,6 +653,7 @@ int launch_partials(pi2_ctx *ctx, const double *costs, int64_t cs_k, int64_t cs_
 // plan_host: also store the updated plan there (see apply_root_kernel)
 int launch_combine(pi2_ctx *ctx, const double *leaves, int64_t n, int N, double neg_inv, double *root,
                    double *plan, cudaStream_t st, bool after_kernel = false, double *plan_host = nullptr) {
+  Range range_("combine");
   if (n == 1 && !root && plan) {  // a single partial: just apply it
     TRY(launch_pdl_if(after_kernel, ctx, apply_root_kernel, dim3((4 * N + 127) / 128), dim3(128), 0, st, leaves, N, plan, ctx->dp, plan_host));
     CU(cudaGetLastError());
@@ -938,6 +955,7 @@ int pi2_set_cost_obstacles(pi2_ctx *ctx, int32_t n, const float *xy) {
 int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan, const double *noise_dev,
                         const float *dyn_dev, double ceiling, double *costs_dev, uint8_t *crash_dev,
                         void *stream) {
+  Range range_("pi2_evaluate_device");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   if (!state || !plan || !noise_dev || !costs_dev || !crash_dev)
@@ -956,6 +974,7 @@ int pi2_evaluate_device(pi2_ctx *ctx, const double *state, const double *plan, c
 
 int pi2_evaluate_device_noise(pi2_ctx *ctx, const double *state, const double *plan, const pi2_optimize_args *args,
                               int32_t iteration, double *costs_dev, uint8_t *crash_dev, void *stream) {
+  Range range_("pi2_evaluate_device_noise");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   TRY(validate_opt(ctx, args));
@@ -973,6 +992,7 @@ int pi2_evaluate_device_noise(pi2_ctx *ctx, const double *state, const double *p
 
 int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const double *noise,
                  const float *dyn, double ceiling, double *costs_out, uint8_t *crash_out) {
+  Range range_("pi2_evaluate");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   if (!state || !plan || !noise || !costs_out || !crash_out) return fail(ctx, PI2_ERR_INVALID, "null argument");
@@ -1000,6 +1020,7 @@ int pi2_evaluate(pi2_ctx *ctx, const double *state, const double *plan, const do
 
 int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const double *costs_dev,
                       const double *noise_dev, double temperature, double *plan_out, void *stream) {
+  Range range_("pi2_update_device");
   if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
   TRY(bind(ctx));
   if (!ctx->have_dyn) return fail(ctx, PI2_ERR_STATE, "dynamics not set (pi2_set_dynamics)");
@@ -1024,6 +1045,7 @@ int pi2_update_device(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, co
 
 int pi2_update(pi2_ctx *ctx, int64_t K, int32_t N, const double *plan, const double *costs,
                const double *noise, double temperature, double *plan_out) {
+  Range range_("pi2_update");
   if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
   TRY(bind(ctx));
   if (K < 1 || N < 1 || !costs || !noise) return fail(ctx, PI2_ERR_INVALID, "batch does not match plan dimensions");
@@ -1089,6 +1111,7 @@ static int run_iterations(pi2_ctx *ctx, const pi2_optimize_args *args, cudaStrea
 }
 
 int pi2_iterate_device(pi2_ctx *ctx, const pi2_optimize_args *args, void *stream) {
+  Range range_("pi2_iterate_device");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   TRY(validate_opt(ctx, args));
@@ -1100,6 +1123,7 @@ int pi2_iterate_device(pi2_ctx *ctx, const pi2_optimize_args *args, void *stream
 }
 
 int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi2_optimize_args *args) {
+  Range range_("pi2_optimize");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   TRY(validate_opt(ctx, args));
@@ -1119,6 +1143,7 @@ int pi2_optimize(pi2_ctx *ctx, const double *state, double *plan_inout, const pi
 
 int pi2_receding_horizon_step(pi2_ctx *ctx, const double *state, double *plan_inout,
                               const pi2_optimize_args *args, double *control_out) {
+  Range range_("pi2_receding_horizon_step");
   TRY(pi2_optimize(ctx, state, plan_inout, args));
   const int N = ctx->N;
   if (control_out) std::memcpy(control_out, plan_inout, 4 * sizeof(double));
@@ -1147,6 +1172,7 @@ int pi2_read_plan(pi2_ctx *ctx, double *plan_out, void *stream) {
 
 int pi2_iterate_local(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t iteration, double *root_dev,
                       void *stream) {
+  Range range_("pi2_iterate_local");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   TRY(validate_opt(ctx, args));
@@ -1190,6 +1216,7 @@ int pi2_enqueue_pull(pi2_ctx *ctx, void *stream) {
 }
 
 int pi2_iterate_local_staged(pi2_ctx *ctx, int32_t iteration, double temperature, double *root_dev, void *stream) {
+  Range range_("pi2_iterate_local_staged");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   if (iteration < 0 || !root_dev) return fail(ctx, PI2_ERR_INVALID, "bad iteration index or null partial buffer");
@@ -1238,6 +1265,7 @@ int pi2_fused_step(pi2_ctx *ctx, int32_t *sub_rollouts_out) {
 }
 
 int pi2_profile_iteration(pi2_ctx *ctx, const pi2_optimize_args *args, int32_t reps, double *stage_ms) {
+  Range range_("pi2_profile_iteration");
   TRY(check_ready(ctx));
   TRY(bind(ctx));
   TRY(validate_opt(ctx, args));
@@ -1309,6 +1337,7 @@ int pi2_profile_evaluate(pi2_ctx *ctx, const double *state, const double *plan, 
 
 int pi2_iterate_finalize(pi2_ctx *ctx, const double *gathered, int32_t world, double temperature,
                          void *stream) {
+  Range range_("pi2_iterate_finalize");
   if (!ctx || !gathered || world < 1) return fail(ctx, PI2_ERR_INVALID, "bad gathered partials");
   TRY(bind(ctx));
   if (!(temperature > 0)) return fail(ctx, PI2_ERR_INVALID, "temperature must be positive");
@@ -1372,6 +1401,7 @@ int pi2_combine_partials_host(const double *partials, int64_t count, int32_t N, 
 
 int pi2_device_noise(pi2_ctx *ctx, int32_t which, uint64_t seed, uint64_t cycle, uint64_t iteration,
                      const double *std_, void *out_host) {
+  Range range_("pi2_device_noise");
   if (!ctx || !out_host) return fail(ctx, PI2_ERR_INVALID, "null argument");
   if (which != PI2_STREAM_CONTROL && which != PI2_STREAM_DYNAMICS)
     return fail(ctx, PI2_ERR_INVALID, "unknown noise stream %d", which);
@@ -1406,6 +1436,7 @@ int pi2_device_noise(pi2_ctx *ctx, int32_t which, uint64_t seed, uint64_t cycle,
 
 int pi2_lwpr_predict(pi2_ctx *ctx, int32_t axis, int64_t rows, const float *X, float *mean_out,
                      float *var_out) {
+  Range range_("pi2_lwpr_predict");
   if (!ctx) return fail(nullptr, PI2_ERR_INVALID, "null context");
   if (axis < 0 || axis > 2 || ctx->axes[axis].L == 0) return fail(ctx, PI2_ERR_INVALID, "no receptive fields");
   if (rows < 1 || !X || !mean_out) return fail(ctx, PI2_ERR_INVALID, "X must have shape (B, input_dim)");

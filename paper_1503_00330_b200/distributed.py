@@ -45,7 +45,9 @@ def gather_partials(partial, group=None):
     world = dist.get_world_size(group)
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
+        torch.cuda.nvtx.range_push("gather_partials")  # NVTX, like the C ABI's entry points
         dist.all_gather_into_tensor(out, partial.contiguous(), group=group)
+        torch.cuda.nvtx.range_pop()
         return out
     host = partial.detach().to("cpu")  # synchronises with the kernels that wrote it
     parts = [torch.empty_like(host) for _ in range(world)]
