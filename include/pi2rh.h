@@ -67,7 +67,7 @@ typedef struct pi2_dims {
   int64_t num_rollouts;       /* K of this context                      */
   int64_t rollout_offset;     /* global index of its first rollout      */
   int64_t num_rollouts_total; /* global K (0 = num_rollouts)            */
-  int32_t horizon_steps;      /* N (<= 2^24; memory is the real bound)  */
+  int32_t horizon_steps;      /* N (<= 524280)                          */
   int32_t sub_rollouts;       /* M (1..PI2_MAX_SUB_ROLLOUTS)            */
 } pi2_dims;
 

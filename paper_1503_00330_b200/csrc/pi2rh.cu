@@ -735,7 +735,10 @@ int pi2_create(int32_t device, const pi2_dims *dims, pi2_ctx **out) {
     return fail(nullptr, PI2_ERR_INVALID, "num_rollouts, sub_rollouts, horizon_steps must be >= 1");
   if (dims->sub_rollouts > PI2_MAX_SUB_ROLLOUTS)
     return fail(nullptr, PI2_ERR_INVALID, "sub_rollouts must be <= %d", PI2_MAX_SUB_ROLLOUTS);
-  if (dims->horizon_steps > (1 << 24)) return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= %d", 1 << 24);
+  // the partials grid has ceil(N / kChunkWarps) rows (grid.y <= 65535)
+  constexpr int kHorizonLimit = kChunkWarps * 65535;
+  if (dims->horizon_steps > kHorizonLimit)
+    return fail(nullptr, PI2_ERR_INVALID, "horizon_steps must be <= %d", kHorizonLimit);
   if (dims->rollout_offset < 0) return fail(nullptr, PI2_ERR_INVALID, "rollout_offset must be >= 0");
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {

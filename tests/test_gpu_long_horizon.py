@@ -1,4 +1,4 @@
-"""Horizons past 400 steps (the reference has no cap; neither has this engine, short of memory).
+"""Horizons past 400 steps (the reference has no cap; this engine takes up to 524 280).
 
 Above PI2_SMEM_HORIZON (400) the rollout kernels keep each rollout's stage costs in
 a global (N, K) scratch instead of their blocks' shared memory, and the
@@ -90,8 +90,8 @@ def test_long_horizon_device_step():
 
 
 def test_horizon_limit():
-    """Past 4096 steps is fine (test_long_horizon_matches_oracle); the only bound is 2^24."""
+    """Past 4096 steps is fine (test_long_horizon_matches_oracle); the bound is 8 x 65535."""
     from paper_1503_00330_b200 import _abi
 
     with pytest.raises(ValueError, match="horizon_steps"):
-        _abi.Context(0, 16, (1 << 24) + 1, 1)
+        _abi.Context(0, 16, 8 * 65535 + 1, 1)
