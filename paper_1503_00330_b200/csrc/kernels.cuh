@@ -1066,13 +1066,20 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
   for (int j = 0; j < SPL; ++j) any = any || crashed[j];
   const unsigned ballot = __ballot_sync(0xffffffffu, any);
   const unsigned gmask = (GL == 32) ? 0xffffffffu : (((1u << GL) - 1u) << ((threadIdx.x % 32) / GL * GL));
-  bool crash = (ballot & gmask) != 0;
-  if (!live || lane_g != 0) return;
+  // the float64 suffix sums run on the block's first RPB threads, one rollout each (the
+  // lanes of the first warps rather than lane 0 of every group: 1/GL of the issue slots)
+  __shared__ bool scrash[RPB];
+  if (lane_g == 0) scrash[grp] = (ballot & gmask) != 0;
+  __syncthreads();  // stage costs (shared memory or the global scratch) and crash flags
+  const int r = (int)threadIdx.x;
+  const int64_t kr = (int64_t)blockIdx.x * RPB + r;
+  if (r >= RPB || kr >= a.K) return;
+  bool crash = scrash[r];
   const double dt = a.dp.dt, ceiling = sa->ceiling;
   double acc = 0.0;
-  double *out = a.costs + k;  // t-major: S(k, t) at out[t * K]
+  double *out = a.costs + kr;  // t-major: S(k, t) at out[t * K]
   for (int t = N - 1; t >= 0; --t) {
-    const double s = __dmul_rn((double)(a.qs ? a.qs[(int64_t)t * a.K + k] : sq[t * RPB + grp]), dt);
+    const double s = __dmul_rn((double)(a.qs ? a.qs[(int64_t)t * a.K + kr] : sq[t * RPB + r]), dt);
     acc = (t == N - 1) ? s : __dadd_rn(acc, s);
     double v = acc;
     if (!isfinite(v)) {
@@ -1081,7 +1088,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
     }
     out[(int64_t)t * a.K] = v;
   }
-  a.crash[k] = crash ? 1 : 0;
+  a.crash[kr] = crash ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
