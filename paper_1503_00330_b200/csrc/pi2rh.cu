@@ -27,9 +27,16 @@ namespace {
 // NVTX range (header-only NVTX3: a no-op unless a tool such as ncu --nvtx or nsys is
 // attached): every C-ABI entry point and every stage launch is a named range, so a
 // profiler can filter by them (ncu --nvtx --nvtx-include "lwpr/").
+#ifndef PI2_NVTX
+#define PI2_NVTX 1
+#endif
 struct Range {
-  explicit Range(const char *name) { nvtxRangePushA(name); }
-  ~Range() { nvtxRangePop(); }
+  explicit Range(const char *name) {
+    if (PI2_NVTX) nvtxRangePushA(name);
+  }
+  ~Range() {
+    if (PI2_NVTX) nvtxRangePop();
+  }
   Range(const Range &) = delete;
   Range &operator=(const Range &) = delete;
 };
