@@ -140,6 +140,17 @@ __device__ __forceinline__ double clip_np(double v, double lo, double hi) {
   const double t = (v > lo || v != v) ? v : lo;
   return (t < hi || t != t) ? t : hi;
 }
+// The same for bounds that are not NaN (the host checks, DynParams): !(v <= lo) is
+// (v > lo || v != v) when lo is not NaN -- one unordered compare and a select per bound
+// instead of two compares, a predicate combine and two selects.
+__device__ __forceinline__ double clip_np_nonan(double v, double lo, double hi) {
+  const double t = !(v <= lo) ? v : lo;
+  return !(t >= hi) ? t : hi;
+}
+template <bool NONAN>
+__device__ __forceinline__ double clip_bounds(double v, double lo, double hi) {
+  return NONAN ? clip_np_nonan(v, lo, hi) : clip_np(v, lo, hi);
+}
 
 
 // ---------------------------------------------------------------------------
@@ -156,7 +167,7 @@ __device__ __forceinline__ double clip_np(double v, double lo, double hi) {
 #endif
 constexpr int kAttUnroll = PI2_ATT_UNROLL;
 
-template <bool DEVICE_NOISE>
+template <bool DEVICE_NOISE, bool NONAN = false>
 __global__ void __launch_bounds__(kRolloutBlock)
     attitude_kernel(const StepArgs *__restrict__ sa, const double *__restrict__ plan,
                     const double *__restrict__ eps, int iteration, int64_t K, int64_t k_off, int N,
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(kRolloutBlock)
       double u[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        u[c] = clip_np(__dadd_rn(splan[4 * t + c], e[j][c]), dp.lo[c], dp.hi[c]);
+        u[c] = clip_bounds<NONAN>(__dadd_rn(splan[4 * t + c], e[j][c]), dp.lo[c], dp.hi[c]);
       xk[(int64_t)t * K] = make_float4(__double2float_rn(ang[0]), __double2float_rn(ang[1]),
                           __double2float_rn(ang[2]), __double2float_rn(u[3]));
 #pragma unroll

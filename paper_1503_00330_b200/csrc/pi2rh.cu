@@ -97,6 +97,7 @@ struct pi2_ctx {
   double *d_partials = nullptr, *d_root = nullptr;
   float4 *d_z = nullptr;  // device-noise exploration normals z(k, t) at [t * K + k] (attitude -> partials)
   bool store_z = true;    // PI2_STORE_Z=0: the partials kernel regenerates z instead (experiments)
+  bool bounds_nonan = false;  // no control bound is NaN: the attitude kernel's cheaper clip (pi2_set_dynamics)
   int64_t n_chunks = 0;
   // lazily grown scratch
   double *d_noise = nullptr;
@@ -589,13 +590,15 @@ int launch_rollouts(pi2_ctx *ctx, int iteration, const double *noise_dev, const 
                      ctx->d_ang_last, ctx->store_z ? ctx->d_z : nullptr));
     }
   } else if (noise_dev) {
-    TRY(set_smem(ctx, attitude_kernel<false>, psmem));
-    TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<false>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+    auto *fn = ctx->bounds_nonan ? attitude_kernel<false, true> : attitude_kernel<false, false>;
+    TRY(set_smem(ctx, fn, psmem));
+    TRY(launch_pdl_if(att_pdl, ctx, fn, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
                    noise_dev, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last,
                    nullptr));
   } else {
-    TRY(set_smem(ctx, attitude_kernel<true>, psmem));
-    TRY(launch_pdl_if(att_pdl, ctx, attitude_kernel<true>, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
+    auto *fn = ctx->bounds_nonan ? attitude_kernel<true, true> : attitude_kernel<true, false>;
+    TRY(set_smem(ctx, fn, psmem));
+    TRY(launch_pdl_if(att_pdl, ctx, fn, dim3(grid), dim3(kRolloutBlock), psmem, st, ctx->d_args, ctx->d_plan,
                    nullptr, iteration, K, ctx->dims.rollout_offset, N, ctx->dp, ctx->d_xin, ctx->d_ang_last, ctx->store_z ? ctx->d_z : nullptr));
   }
   CU(cudaGetLastError());
@@ -854,9 +857,11 @@ int pi2_set_dynamics(pi2_ctx *ctx, const pi2_dynamics *d) {
   DynParams &p = ctx->dp;
   p.dt = d->dt;
   p.gain_dt = d->rate_gain * d->dt;
+  ctx->bounds_nonan = true;
   for (int c = 0; c < 4; ++c) {
     p.lo[c] = d->lo[c];
     p.hi[c] = d->hi[c];
+    if (std::isnan(d->lo[c]) || std::isnan(d->hi[c])) ctx->bounds_nonan = false;
   }
   p.dt32 = (float)d->dt;
   p.dt2_32 = p.dt32 * p.dt32;

@@ -149,6 +149,30 @@ def test_many_obstacles_match_oracle(K, M):
         assert cost_rel_err(b.costs_to_go, rc) < COST_RTOL, n_obs
 
 
+@pytest.mark.parametrize("which", ["lo", "hi"])
+def test_nan_control_bound_matches_oracle(which):
+    """A NaN control bound (r_max or f_max NaN) takes the attitude kernel's general clip
+    (NaN-propagating on both operands, numpy's np.clip); the default finite bounds take the
+    cheaper one.  Both follow the oracle: here every clipped control is NaN, so every
+    rollout gets the cost ceiling and a crash."""
+    K, N, L, M = 700, 20, 16, 1
+    stacks = synthetic.hybrid_stacks(L, seed=3)
+    params = P.QuadParams()
+    model = P.HybridModel.from_stacks(stacks, params)
+    cfg = P.PiConfig(num_rollouts=K, sub_rollouts=M, horizon_steps=N, iterations_per_step=1, rng_seed=5)
+    task = P.Task.default()
+    state = P.QuadState.hover(task.spawn)
+    lo, hi = params.control_bounds()
+    (lo if which == "lo" else hi)[1] = np.nan
+    plan = P.ControlPlan(np.tile([0.0, 0.0, 0.0, params.hover_thrust], (N, 1)), params.dt, 0.0, lo, hi)
+    noise = P.sample_noise(cfg, 2, 0)
+    b = P.RolloutEngine(model, cfg, device=0).evaluate(state, plan, noise, P.RolloutCost(task, 1))
+    om = RO.Model(stacks)
+    rc, rf = RO.evaluate(om, state.as_array(), plan.controls, lo, hi, noise, RO.Cost(TASK_WAYPOINTS[1], TASK_OBSTACLES))
+    np.testing.assert_array_equal(b.crash_flags, rf)
+    np.testing.assert_array_equal(b.costs_to_go, rc)
+
+
 def test_frozen_lwpr_predict_matches_reference():
     z = load("lwpr")
     st = stacks_from(z, "diag_")
