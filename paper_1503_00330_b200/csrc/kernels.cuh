@@ -605,6 +605,11 @@ __device__ __forceinline__ float variance_term(float kappa, float3 sd) {
 __device__ __forceinline__ float3 ld_planes(const float *p, int64_t plane, int64_t row) {
   return make_float3(__ldcg(p + row), __ldcg(p + plane + row), __ldcg(p + 2 * plane + row));
 }
+// the same with 32-bit element offsets (3 planes x K x N < 2^32, host-checked: RollArgs::rows32),
+// so each address is one IMAD.WIDE.U32 instead of a 64-bit add chain
+__device__ __forceinline__ float3 ld_planes32(const float *p, uint32_t plane, uint32_t row) {
+  return make_float3(__ldcg(p + row), __ldcg(p + (plane + row)), __ldcg(p + (2u * plane + row)));
+}
 
 __device__ __forceinline__ float sign_of(float v) {  // np.sign (0 -> 0, NaN -> NaN)
   return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : v);
@@ -877,7 +882,7 @@ constexpr int kRollUnroll = PI2_ROLL_UNROLL;
 // suffix sum.
 // FAST: hybrid LWPR model, device dynamics noise, navigation cost (the
 // real-time configuration) with every branch folded at compile time.
-template <int G, bool FAST>
+template <int G, bool FAST, bool R32 = false>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a) {
   constexpr int SPL = G > 32 ? G / 32 : 1;  // sub-rollouts per lane (G = 64 .. 256: 32 lanes)
   constexpr int GL = G / SPL;             // lanes per rollout
@@ -935,18 +940,30 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_group_kernel(RollArgs a
     }
     apn = (1 < N) ? __ldcg(a.xin + a.K + kk) : __ldcg(a.ang_last + kk);
   }
+  const uint32_t plane32 = (uint32_t)a.lw_plane, k32 = (uint32_t)a.K;
+  uint32_t row32 = (uint32_t)kk;  // rows32 path: t * K + k
 #pragma unroll(kRollUnroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + kk;
     const float3 m4 = m4n, s4 = s4n;
     const float4 ap = apn;
     if (active && t + 1 < N) {
-      if (hybrid) {
-        m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
-        s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
+      if (R32) {
+        const uint32_t rn = row32 + k32;
+        if (hybrid) {
+          m4n = ld_planes32(a.lw_mean, plane32, rn);
+          s4n = ld_planes32(a.lw_std, plane32, rn);
+        }
+        apn = (t + 2 < N) ? __ldcg(a.xin + (rn + k32)) : __ldcg(a.ang_last + kk);
+      } else {
+        if (hybrid) {
+          m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
+          s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
+        }
+        apn = (t + 2 < N) ? __ldcg(a.xin + row + 2 * a.K) : __ldcg(a.ang_last + kk);
       }
-      apn = (t + 2 < N) ? __ldcg(a.xin + row + 2 * a.K) : __ldcg(a.ang_last + kk);
     }
+    row32 += k32;
     float q[SPL];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) q[j] = 0.0f;

@@ -390,7 +390,9 @@ int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
 
 template <int G, bool FAST>
 int launch_group_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
-  auto *fn = rollout_group_kernel<G, FAST>;
+  // 32-bit row offsets when every plane element index fits (3 planes x K x N < 2^32)
+  const bool r32 = FAST && 3 * a.lw_plane < (int64_t(1) << 32) && a.K * a.N * 4 < (int64_t(1) << 32);
+  auto *fn = r32 ? rollout_group_kernel<G, FAST, FAST> : rollout_group_kernel<G, FAST, false>;
   constexpr int RPB = kRolloutBlock / (G > 32 ? 32 : G);
   const int smem = a.qs ? 0 : a.N * RPB * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
