@@ -677,7 +677,7 @@ constexpr int kRoll1Unroll = PI2_ROLL1_UNROLL;
 // MM: compile-time sub-rollouts held in registers (1; more than one sub-rollout per
 // rollout runs rollout_group_kernel, up to PI2_MAX_SUB_ROLLOUTS on 32 lanes).
 // FAST: hybrid LWPR model + navigation cost, branches folded at compile time.
-template <int MM, bool FAST>
+template <int MM, bool FAST, bool R32 = false>
 __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   constexpr int MCAP = MM > 0 ? MM : 64;  // MM = 0 (runtime M) is not instantiated: S > 1 runs the group kernel
   extern __shared__ float sq[];  // (N, blockDim): this thread's stage costs, column tid
@@ -737,6 +737,7 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
   }
 #endif
   float4 xr = (model == PI2_MODEL_ANALYTIC) ? __ldcg(a.xin + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t rn32 = (uint32_t)(a.K + k);  // R32: the next step's row index
 #pragma unroll(kRoll1Unroll)
   for (int t = 0; t < N; ++t) {
     const int64_t row = (int64_t)t * a.K + k;
@@ -753,9 +754,17 @@ __global__ void __launch_bounds__(kRolloutBlock) rollout_kernel(RollArgs a) {
     }
 #else
     if (t + 1 < N) {
-      if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
-      if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
-      apn = ap_row(t + 1);
+      if (R32) {  // 32-bit element offsets (see ld_planes32); rn32 = (t + 1) K + k
+        const uint32_t rn = rn32, pl = (uint32_t)a.lw_plane;
+        rn32 += (uint32_t)a.K;
+        if (hybrid) m4n = ld_planes32(a.lw_mean, pl, rn);
+        if (with_std) s4n = ld_planes32(a.lw_std, pl, rn);
+        apn = (t + 2 < N) ? __ldcg(a.xin + (rn + (uint32_t)a.K)) : __ldcg(a.ang_last + k);
+      } else {
+        if (hybrid) m4n = ld_planes(a.lw_mean, a.lw_plane, row + a.K);
+        if (with_std) s4n = ld_planes(a.lw_std, a.lw_plane, row + a.K);
+        apn = ap_row(t + 1);
+      }
     }
 #endif
     float mn[3], sd[3] = {0.0f, 0.0f, 0.0f};

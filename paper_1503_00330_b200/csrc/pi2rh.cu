@@ -379,7 +379,8 @@ bool penalty(const pi2_ctx *ctx) {
 
 template <int MM, bool FAST>
 int launch_rollout_t(pi2_ctx *ctx, const RollArgs &a, cudaStream_t st) {
-  auto *fn = rollout_kernel<MM, FAST>;
+  const bool r32 = FAST && 3 * a.lw_plane < (int64_t(1) << 32) && a.K * a.N * 4 < (int64_t(1) << 32);
+  auto *fn = r32 ? rollout_kernel<MM, FAST, FAST> : rollout_kernel<MM, FAST, false>;
   const int smem = a.qs ? 0 : a.N * kRolloutBlock * (int)sizeof(float);
   TRY(set_smem(ctx, fn, smem));
   const int64_t grid = (a.K + kRolloutBlock - 1) / kRolloutBlock;
